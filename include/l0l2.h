@@ -1,0 +1,181 @@
+/*
+ * l0l2.h — C-ABI of the B200 (sm_100a) library for the data-parallel hot path of the
+ * ℓ0–ℓ2 branch-and-bound of arXiv 2602.04551 (PAPER.md, cited as P:<line>).
+ *
+ *   problem (eq:original; Big-M perspective MIP eq:perspective):
+ *       min_β ½‖y − Xβ‖² + λ0‖β‖₀ + λ2‖β‖²   s.t. ‖β‖∞ ≤ M
+ *
+ * Conventions shared by every entry point
+ *   - All floating point is IEEE float64.  X is n×p COLUMN-major (column j = feature j,
+ *     contiguous, leading dimension n).  Index arrays are 0-based int32 unless stated.
+ *   - Return value: 0 = OK; negative = hard failure (L0L2_E*); positive = soft warning
+ *     (L0L2_W*) whose outputs are still valid.  l0l2_last_error() gives a message.
+ *   - A ctx owns all device memory it allocates and is bound to one CUDA device.  It is
+ *     not thread-safe; separate ctxs (one per GPU / process) are independent.
+ *   - No CPU fallback exists: every numeric step runs in this library's sm_100a kernels.
+ *     Without a usable CUDA device l0l2_create returns L0L2_ECUDA.
+ */
+#ifndef L0L2_H_
+#define L0L2_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define L0L2_OK          0
+#define L0L2_EINVAL    (-1)   /* bad argument: n,p ≤ 0; λ2 ≤ 0; λ0 < 0; M ≤ 0; ρ < 0;
+                                 F0 ∩ F1 ≠ ∅; index out of range; NaN/Inf in X or y */
+#define L0L2_ENOMEM    (-2)   /* device or host allocation failed */
+#define L0L2_ECUDA     (-3)   /* CUDA runtime error / no device */
+#define L0L2_ENCCL     (-4)   /* NCCL error, or libnccl.so.2 not loadable */
+#define L0L2_WNOTCONV    1    /* a node hit max_iters; its bound is still valid */
+#define L0L2_WLIMIT      2    /* time or node limit reached; bounds are valid */
+
+/* node flags (bit set) returned by l0l2_bound_batch */
+#define L0L2_FLAG_CONVERGED 1u  /* relative primal-dual gap ≤ node_tol at a check */
+#define L0L2_FLAG_INTEGRAL  2u  /* every free ẑ within int_tol of {0,1} (P:258 prune (i)) */
+#define L0L2_FLAG_MAXITER   4u  /* stopped at max_iters */
+
+typedef struct l0l2_ctx l0l2_ctx;
+
+/* Options of the node relaxation (ADMM) and of the data placement. */
+typedef struct {
+  double  M;            /* Big-M box bound > 0; required, no default in the paper */
+  double  rho;          /* ADMM penalty ρ > 0; 0 → mean_j ‖X_j‖² (R5)        */
+  double  node_tol;     /* node stop: (P(β) − LB)/max(1,|P|) ≤ node_tol; default 1e-4;
+                           a negative value disables the test (fixed-iteration mode)            */
+  double  int_tol;      /* integrality tolerance on ẑ; default 1e-4                      */
+  int32_t check_every;  /* dual/primal check cadence in iterations; default 10          */
+  int32_t max_iters;    /* ADMM iteration cap per node; default 10000                    */
+  int32_t device;       /* CUDA device ordinal                                                   */
+  int32_t x_on_device;  /* 1: X, y passed to l0l2_create are device pointers on `device`        */
+} l0l2_opts;
+
+/* Fill `o` with the defaults above (M = 0 must then be set by the caller). */
+void l0l2_default_opts(l0l2_opts* o);
+
+/*
+ * l0l2_create — copy (X, y) to HBM and run the tree-wide precompute:
+ *   c = Xᵀy, colsq_j = ‖X_j‖², A = XXᵀ + ρI_n = LLᵀ (Cholesky), Z = L⁻¹X (n×p).
+ * D = (XᵀX+ρI)⁻¹ = (I − ZᵀZ)/ρ is then applied implicitly (Woodbury, P:375 with the 1/ρ²
+ * typo corrected, R1).  X and y are copied (host or device per opts->x_on_device)
+ * and never aliased afterwards.  Errors: L0L2_EINVAL (see above), L0L2_ENOMEM, L0L2_ECUDA.
+ * On error *out is NULL.
+ */
+int l0l2_create(const double* X, const double* y, int64_t n, int64_t p,
+                double lambda0, double lambda2, const l0l2_opts* opts, l0l2_ctx** out);
+
+/*
+ * l0l2_bound_batch — lower bounds of B open nodes at once (batched ADMM).
+ *
+ * Node k has fixings F0 (z=0) and F1 (z=1): entries fix_idx[fix_off[k] .. fix_off[k+1])
+ * with fix_val 0 → F0, 1 → F1.  Every node runs ADMM on eq:ADMM1 with the closed-form
+ * updates eq:b_update, eq:minbetalower and eq:v_i-update,
+ * warm-started from warm_in or cold (zeros).  Every check_every iterations the dual
+ * bound of Proposition 1 is evaluated at r̂ = y − X b̂ and the primal objective of
+ * eq:relaxnode2 at β; the node stops when the relative gap ≤ node_tol.
+ *
+ * ALL array arguments are DEVICE pointers on the ctx device (e.g. torch CUDA tensors),
+ * ordered on `stream` (cudaStream_t, NULL = legacy default stream):
+ *   in   fix_off   int64[B+1]        CSR offsets into fix_idx / fix_val
+ *   in   fix_idx   int32[nnz]        coordinate indices, 0 ≤ idx < p, disjoint F0/F1 per node
+ *   in   fix_val   uint8[nnz]        0 → F0, 1 → F1
+ *   in   warm_in   double[B][2][p]   parent (β, v) per node, or NULL for cold starts
+ *   in   parent_lb double[B]         inherited bounds, or NULL (−∞)
+ *   out  lb        double[B]         max(best checked dual, parent_lb)  — a valid lower bound
+ *   out  primal    double[B]         P(β) at the last check (upper bound of the relaxation)
+ *   out  warm_out  double[B][2][p]   final (β, v) for the children, or NULL
+ *   out  zhat      double[B][p]      ẑ recovered from β, or NULL
+ *   out  dual_r    double[B][n]      r̂ = y − X b̂ at the last check, or NULL
+ *   out  branch_j  int32[B]          most fractional free j (ties: larger |β_j|, lower j), −1 if integral
+ *   out  iters     int32[B]          ADMM iterations run
+ *   out  flags     uint8[B]          L0L2_FLAG_* bits
+ * Returns L0L2_WNOTCONV if any node stopped at max_iters (its lb is still valid).
+ * The per-node arithmetic is independent of B and of the other nodes (bitwise).
+ */
+int l0l2_bound_batch(l0l2_ctx* ctx, int32_t B,
+                     const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
+                     const double* warm_in, const double* parent_lb,
+                     double* lb, double* primal, double* warm_out, double* zhat, double* dual_r,
+                     int32_t* branch_j, int32_t* iters, uint8_t* flags, void* stream);
+
+/*
+ * l0l2_upper_batch — feasible objectives on B candidate supports.
+ * For support S_k = supp_idx[supp_off[k] .. supp_off[k+1]) (sorted, distinct) minimise
+ * eq:upperboundbeta U_S(β) = ½‖y − X_Sβ‖² + λ2‖β‖² s.t. |β_i| ≤ M by the fast proximal
+ * gradient method with Nesterov extrapolation t/(t+3) and Armijo backtracking
+ * (eq:fpg_extrapolate..eq:fpg_armijo), batched one CTA per support.
+ * DEVICE pointers, ordered on `stream`:
+ *   in  supp_off int64[B+1], supp_idx int32[nnz]
+ *   out obj      double[B]     U_S(β) + λ0|S|  (objective of eq:perspective at z = 1_S)
+ *   out beta_s   double[nnz]   β_S aligned with supp_idx (may be NULL)
+ */
+int l0l2_upper_batch(l0l2_ctx* ctx, int32_t B, const int64_t* supp_off, const int32_t* supp_idx,
+                     double* obj, double* beta_s, void* stream);
+
+/* Options of the branch-and-bound driver (Algorithm 1). */
+typedef struct {
+  double  gap_tol;          /* stop when (UB − LB)/UB ≤ gap_tol; default 1e-2   */
+  double  time_limit_s;     /* ≤ 0: none                                                          */
+  int64_t node_limit;       /* ≤ 0: none                                                          */
+  int32_t batch;            /* B = nodes per round (the paper's K); default 16            */
+  int32_t rebalance_every;  /* multi-GPU: rounds between frontier rebalancing; default 8         */
+  int64_t warm_bytes_cap;   /* device bytes for parent warm states; 0 → 25% of free HBM          */
+  int32_t verbose;          /* 1: one progress line per round on stderr                          */
+} l0l2_solve_opts;
+
+void l0l2_default_solve_opts(l0l2_solve_opts* o);
+
+typedef struct {
+  int64_t nodes;            /* node relaxations solved (this rank)                               */
+  int64_t node_iters;       /* Σ ADMM iterations over solved nodes (this rank)                   */
+  int64_t rounds;           /* synchronous rounds                                                */
+  int64_t max_open;         /* largest open-node count seen (this rank)                          */
+  int64_t nodes_global;     /* Σ nodes over ranks                                                */
+  int64_t node_iters_global;
+  double  t_total, t_bound, t_upper, t_tree, t_comm;   /* seconds                              */
+  double  lb, ub, gap;      /* certified global bounds at return                                 */
+  int32_t status;           /* 0 optimal (queue exhausted), 1 gap reached, 2 node limit, 3 time limit */
+  int32_t support_size;
+} l0l2_stats;
+
+/*
+ * l0l2_solve — certified best-first BnB (Algorithm 1, batched reading DESIGN.md R9).
+ * Rounds: select ≤ B open nodes by (LB, id); l0l2_bound_batch on them (warm
+ * started from the parent state kept in HBM); l0l2_upper_batch on the rounded supports
+ * F1 ∪ {free: ẑ ≥ ½}; incumbent update; prune by LB ≥ UB(1−1e-12) or integral ẑ
+ * (P:258); branch on the most fractional coordinate (R10).
+ * With a communicator (l0l2_comm_init) the frontier is partitioned across ranks and the
+ * incumbent / global LB / termination are exchanged every round over NCCL.
+ * HOST outputs: beta double[p] (β*, zeros off the support), obj (UB), gap ((UB−LB)/UB);
+ * stats may be NULL.  Every rank returns the same beta, obj and gap.
+ * Returns L0L2_WLIMIT when a time/node limit stopped the search (bounds still valid).
+ */
+int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts, double* beta, double* obj, double* gap,
+               l0l2_stats* stats);
+
+/* Multi-GPU, one process per GPU (torch.distributed provides the process group and
+ * broadcasts the id bytes).  NCCL is loaded at run time (libnccl.so.2).             */
+int l0l2_nccl_unique_id(uint8_t out[128]);
+int l0l2_comm_init(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id[128]);
+
+/* Frontier rebalancing plan used by l0l2_solve every rebalance_every rounds (pure host logic,
+ * exported for tests).  counts[r] = open nodes on rank r.  While the emptiest rank holds fewer
+ * than `batch` nodes and the fullest holds ≥ 2 more, move half the difference (ties → lowest
+ * rank).  Writes up to max_moves triples (src, dst, k) into plan; returns the number of moves
+ * (which may exceed max_moves), or −1 on bad arguments. */
+int l0l2_rebalance_plan(int32_t nranks, const int64_t* counts, int64_t batch, int64_t* plan, int32_t max_moves);
+
+/* Introspection: n, p, ρ actually used, device bytes held, and kernel launches so far. */
+int l0l2_info(const l0l2_ctx* ctx, int64_t* n, int64_t* p, double* rho, int64_t* device_bytes,
+              int64_t* kernel_launches);
+
+const char* l0l2_last_error(const l0l2_ctx* ctx);
+void l0l2_destroy(l0l2_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* L0L2_H_ */

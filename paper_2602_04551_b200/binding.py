@@ -1,0 +1,284 @@
+"""ctypes binding of include/l0l2.h — same names as the C entry points, marshalling only."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(HERE, "libl0l2.so")
+
+OK, EINVAL, ENOMEM, ECUDA, ENCCL = 0, -1, -2, -3, -4
+WNOTCONV, WLIMIT = 1, 2
+FLAG_CONVERGED, FLAG_INTEGRAL, FLAG_MAXITER = 1, 2, 4
+
+
+class L0L2Error(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("l0l2 error %d: %s" % (code, msg))
+        self.code = code
+
+
+class _Opts(C.Structure):
+    _fields_ = [("M", C.c_double), ("rho", C.c_double), ("node_tol", C.c_double), ("int_tol", C.c_double),
+                ("check_every", C.c_int32), ("max_iters", C.c_int32), ("device", C.c_int32),
+                ("x_on_device", C.c_int32)]
+
+
+class _SolveOpts(C.Structure):
+    _fields_ = [("gap_tol", C.c_double), ("time_limit_s", C.c_double), ("node_limit", C.c_int64),
+                ("batch", C.c_int32), ("rebalance_every", C.c_int32), ("warm_bytes_cap", C.c_int64),
+                ("verbose", C.c_int32)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("nodes", C.c_int64), ("node_iters", C.c_int64), ("rounds", C.c_int64), ("max_open", C.c_int64),
+                ("nodes_global", C.c_int64), ("node_iters_global", C.c_int64),
+                ("t_total", C.c_double), ("t_bound", C.c_double), ("t_upper", C.c_double), ("t_tree", C.c_double),
+                ("t_comm", C.c_double), ("lb", C.c_double), ("ub", C.c_double), ("gap", C.c_double),
+                ("status", C.c_int32), ("support_size", C.c_int32)]
+
+
+_lib = None
+P = C.c_void_p
+
+
+def lib_path():
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libl0l2.so (fails loudly if it has not been built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError("libl0l2.so not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(no CPU fallback exists)")
+    lib = C.CDLL(_LIB_PATH, mode=C.RTLD_GLOBAL)
+    lib.l0l2_default_opts.argtypes = [C.POINTER(_Opts)]
+    lib.l0l2_default_opts.restype = None
+    lib.l0l2_create.argtypes = [P, P, C.c_int64, C.c_int64, C.c_double, C.c_double, C.POINTER(_Opts), C.POINTER(P)]
+    lib.l0l2_create.restype = C.c_int
+    lib.l0l2_bound_batch.argtypes = [P, C.c_int32] + [P] * 13 + [P]
+    lib.l0l2_bound_batch.restype = C.c_int
+    lib.l0l2_upper_batch.argtypes = [P, C.c_int32, P, P, P, P, P]
+    lib.l0l2_upper_batch.restype = C.c_int
+    lib.l0l2_default_solve_opts.argtypes = [C.POINTER(_SolveOpts)]
+    lib.l0l2_default_solve_opts.restype = None
+    lib.l0l2_solve.argtypes = [P, C.POINTER(_SolveOpts), P, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                               C.POINTER(_Stats)]
+    lib.l0l2_solve.restype = C.c_int
+    lib.l0l2_nccl_unique_id.argtypes = [P]
+    lib.l0l2_nccl_unique_id.restype = C.c_int
+    lib.l0l2_comm_init.argtypes = [P, C.c_int32, C.c_int32, P]
+    lib.l0l2_comm_init.restype = C.c_int
+    lib.l0l2_rebalance_plan.argtypes = [C.c_int32, P, C.c_int64, P, C.c_int32]
+    lib.l0l2_rebalance_plan.restype = C.c_int
+    lib.l0l2_info.argtypes = [P] + [P] * 5
+    lib.l0l2_info.restype = C.c_int
+    lib.l0l2_last_error.argtypes = [P]
+    lib.l0l2_last_error.restype = C.c_char_p
+    lib.l0l2_destroy.argtypes = [P]
+    lib.l0l2_destroy.restype = None
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    """Names of the l0l2_* functions declared in include/l0l2.h that the library exports."""
+    import re
+    hdr = open(os.path.join(HERE, "..", "include", "l0l2.h")).read()
+    names = sorted(set(re.findall(r"\b(l0l2_[a-z_0-9]+)\s*\(", hdr)))
+    lib = load_library()
+    return {n: hasattr(lib, n) for n in names}
+
+
+def _check(rc, ctx=None, allow_warn=True):
+    if rc < 0 or (rc > 0 and not allow_warn):
+        msg = load_library().l0l2_last_error(ctx).decode(errors="replace")
+        raise L0L2Error(rc, msg)
+    return rc
+
+
+def rebalance_plan(counts, batch, max_moves=64):
+    lib = load_library()
+    cnt = np.ascontiguousarray(counts, dtype=np.int64)
+    plan = np.zeros(3 * max_moves, dtype=np.int64)
+    m = lib.l0l2_rebalance_plan(len(cnt), cnt.ctypes.data, int(batch), plan.ctypes.data, max_moves)
+    if m < 0:
+        raise L0L2Error(m, "bad arguments")
+    return [tuple(int(x) for x in plan[3 * i:3 * i + 3]) for i in range(min(m, max_moves))]
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(load_library().l0l2_nccl_unique_id(C.cast(buf, P)))
+    return bytes(buf)
+
+
+def _ptr(t):
+    """Device pointer of a torch CUDA tensor (or None → NULL)."""
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+class Problem:
+    """One l0l2_ctx: (X, y, λ0, λ2, M) resident in HBM with the tree-wide precompute done.
+
+    X: numpy float64 (n×p; any order — copied column-major) or a torch CUDA float64 tensor in
+    column-major layout (X.T contiguous); y likewise.
+    """
+
+    def __init__(self, X, y, lambda0, lambda2, M, rho=0.0, node_tol=1e-4, int_tol=1e-4, check_every=10,
+                 max_iters=10000, device=0):
+        self._lib = load_library()
+        o = _Opts()
+        self._lib.l0l2_default_opts(C.byref(o))
+        o.M, o.rho, o.node_tol, o.int_tol = float(M), float(rho), float(node_tol), float(int_tol)
+        o.check_every, o.max_iters, o.device = int(check_every), int(max_iters), int(device)
+        self._keep = []
+        if isinstance(X, np.ndarray):
+            Xf = np.asfortranarray(X, dtype=np.float64)
+            yf = np.ascontiguousarray(y, dtype=np.float64)
+            n, p = Xf.shape
+            o.x_on_device = 0
+            xp, yp = Xf.ctypes.data, yf.ctypes.data
+            self._keep += [Xf, yf]
+        else:   # torch CUDA tensors
+            import torch
+            assert X.is_cuda and X.dtype == torch.float64
+            n, p = X.shape
+            if not X.T.is_contiguous():
+                X = X.T.contiguous().T
+            yv = y.contiguous()
+            o.x_on_device = 1
+            xp, yp = X.data_ptr(), yv.data_ptr()
+            self._keep += [X, yv]
+        self.n, self.p = int(n), int(p)
+        self.lambda0, self.lambda2, self.M = float(lambda0), float(lambda2), float(M)
+        ctx = P()
+        rc = self._lib.l0l2_create(C.c_void_p(xp), C.c_void_p(yp), self.n, self.p, self.lambda0, self.lambda2,
+                                   C.byref(o), C.byref(ctx))
+        self._keep = []
+        if rc != OK:
+            raise L0L2Error(rc, self._lib.l0l2_last_error(None).decode(errors="replace"))
+        self._ctx = ctx
+        self.device = int(device)
+
+    # -------------------------------------------------------------- lifecycle / info
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self._lib.l0l2_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self):
+        n, p, dev, launches = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        rho = C.c_double()
+        _check(self._lib.l0l2_info(self._ctx, C.byref(n), C.byref(p), C.byref(rho), C.byref(dev), C.byref(launches)),
+               self._ctx)
+        return dict(n=n.value, p=p.value, rho=rho.value, device_bytes=dev.value, kernel_launches=launches.value)
+
+    @property
+    def rho(self):
+        return self.info()["rho"]
+
+    # -------------------------------------------------------------- batch calls (device tensors)
+    def fixings_csr(self, fixings):
+        """[(F0, F1), ...] → (fix_off int64[B+1], fix_idx int32, fix_val uint8) CUDA tensors."""
+        import torch
+        off, idx, val = [0], [], []
+        for F0, F1 in fixings:
+            F0 = [int(i) for i in F0]
+            F1 = [int(i) for i in F1]
+            idx += F0 + F1
+            val += [0] * len(F0) + [1] * len(F1)
+            off.append(len(idx))
+        dev = torch.device("cuda", self.device)
+        return (torch.tensor(off, dtype=torch.int64, device=dev),
+                torch.tensor(idx if idx else [0], dtype=torch.int32, device=dev),
+                torch.tensor(val if val else [0], dtype=torch.uint8, device=dev))
+
+    def l0l2_bound_batch(self, fixings, warm_in=None, parent_lb=None, want_warm=True, want_zhat=False,
+                         want_dual_r=False, stream=None):
+        import torch
+        B = len(fixings)
+        dev = torch.device("cuda", self.device)
+        fo, fi, fv = self.fixings_csr(fixings)
+        f64 = dict(dtype=torch.float64, device=dev)
+        out = dict(lb=torch.empty(B, **f64), primal=torch.empty(B, **f64),
+                   branch_j=torch.empty(B, dtype=torch.int32, device=dev),
+                   iters=torch.empty(B, dtype=torch.int32, device=dev),
+                   flags=torch.empty(B, dtype=torch.uint8, device=dev))
+        out["warm_out"] = torch.empty((B, 2, self.p), **f64) if want_warm else None
+        out["zhat"] = torch.empty((B, self.p), **f64) if want_zhat else None
+        out["dual_r"] = torch.empty((B, self.n), **f64) if want_dual_r else None
+        if warm_in is not None:
+            warm_in = warm_in.to(**f64).contiguous()
+        if parent_lb is not None:
+            parent_lb = torch.as_tensor(parent_lb, **f64).contiguous()
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        rc = self._lib.l0l2_bound_batch(self._ctx, B, _ptr(fo), _ptr(fi), _ptr(fv), _ptr(warm_in), _ptr(parent_lb),
+                                        _ptr(out["lb"]), _ptr(out["primal"]), _ptr(out["warm_out"]),
+                                        _ptr(out["zhat"]), _ptr(out["dual_r"]), _ptr(out["branch_j"]),
+                                        _ptr(out["iters"]), _ptr(out["flags"]), C.c_void_p(s.cuda_stream))
+        _check(rc, self._ctx)
+        out["rc"] = rc
+        return out
+
+    def l0l2_upper_batch(self, supports, stream=None):
+        import torch
+        dev = torch.device("cuda", self.device)
+        off, idx = [0], []
+        for S in supports:
+            idx += [int(i) for i in S]
+            off.append(len(idx))
+        so = torch.tensor(off, dtype=torch.int64, device=dev)
+        si = torch.tensor(idx if idx else [0], dtype=torch.int32, device=dev)
+        obj = torch.empty(len(supports), dtype=torch.float64, device=dev)
+        bs = torch.empty(max(1, len(idx)), dtype=torch.float64, device=dev)
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        _check(self._lib.l0l2_upper_batch(self._ctx, len(supports), _ptr(so), _ptr(si), _ptr(obj), _ptr(bs),
+                                          C.c_void_p(s.cuda_stream)), self._ctx)
+        betas = []
+        bsh = bs.cpu().numpy()
+        for k in range(len(supports)):
+            betas.append(bsh[off[k]:off[k + 1]].copy())
+        return obj, betas
+
+    # -------------------------------------------------------------- solve / multi-GPU
+    def l0l2_comm_init(self, nranks, rank, uid: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(self._lib.l0l2_comm_init(self._ctx, int(nranks), int(rank), C.cast(buf, P)), self._ctx)
+
+    def init_distributed(self):
+        """Build the NCCL communicator from the current torch.distributed process group."""
+        import torch.distributed as dist
+        if not dist.is_initialized() or dist.get_world_size() == 1:
+            return
+        obj = [nccl_unique_id() if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        self.l0l2_comm_init(dist.get_world_size(), dist.get_rank(), obj[0])
+
+    def l0l2_solve(self, gap_tol=1e-2, batch=16, time_limit_s=0.0, node_limit=0, rebalance_every=8,
+                   warm_bytes_cap=0, verbose=False):
+        so = _SolveOpts()
+        self._lib.l0l2_default_solve_opts(C.byref(so))
+        so.gap_tol, so.batch, so.time_limit_s = float(gap_tol), int(batch), float(time_limit_s)
+        so.node_limit, so.rebalance_every, so.warm_bytes_cap = int(node_limit), int(rebalance_every), int(warm_bytes_cap)
+        so.verbose = int(bool(verbose))
+        beta = np.zeros(self.p, dtype=np.float64)
+        obj, gap = C.c_double(), C.c_double()
+        st = _Stats()
+        rc = self._lib.l0l2_solve(self._ctx, C.byref(so), beta.ctypes.data, C.byref(obj), C.byref(gap), C.byref(st))
+        _check(rc, self._ctx)
+        stats = {f: getattr(st, f) for f, _ in _Stats._fields_}
+        return dict(beta=beta, obj=obj.value, gap=gap.value, support=np.nonzero(beta)[0], stats=stats, rc=rc)

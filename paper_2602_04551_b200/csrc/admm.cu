@@ -1,0 +1,701 @@
+// Batched ADMM node lower bound (§3.1-§3.2) as ONE persistent,
+// cooperative sm_100a kernel per group of kBC = 8 nodes.
+//
+// Per iteration t and node k (state β, v in HBM, layout [p][kBC] node-minor):
+//   w  = c + ρβ − v                              (eq:b_update)
+//   u  = Z w            (n)   forward  contraction, Z = L⁻¹X  (precompute.cu)
+//   s  = Zᵀ u           (p)   adjoint  contraction
+//   b  = (w − s)/ρ                               (= D w with D = (XᵀX+ρI)⁻¹, Woodbury, R1)
+//   β⁺ = prox(b + v/ρ)                           (eq:minbetalower, R3)
+//   v⁺ = v + ρ(b − β⁺)                           (eq:v_i-update)
+//
+// One-pass mapping: because the prox, the v-update and the next w
+// are elementwise in the coordinate j, one sweep over 8-column tiles Z_J of Z does
+//   adjoint  S_J = Z_Jᵀ u          (DMMA m8n8k4, K = n split over 16 warps)
+//   epilogue b, β⁺, v⁺, w⁺ and the check sums for the 8×8 (column, node) block
+//   forward  u⁺ += Z_J w⁺_J        (DMMA, accumulators in registers)
+// from the SAME shared-memory copy of Z_J (a cp.async.bulk / TMA bulk copy, double buffered
+// with an mbarrier), so Z is read from HBM once per iteration.  The per-CTA forward partials
+// are then reduced across the grid in a fixed order (deterministic, independent of B).
+//
+// Checks (every check_every iterations) use identities that need no pass over X:
+//   Xᵀr̂ = c − s,  ‖X b‖² = bᵀs   ⇒  dual(r̂ = y − Xb) = ½‖y‖² − ½ bᵀs − Σ ν_j(|c_j − s_j|)
+//   primal P(β) = ½‖y‖² − cᵀβ + ½‖L(Zβ)‖² + Σ ψ_j(β_j)
+// where Zβ is one extra forward-only sweep on check iterations.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace l0l2 {
+namespace {
+
+constexpr int NW = kAdmmThreads / 32;   // 16 warps
+constexpr int MAXMT = 9;                // ≤ 9 row tiles of 8 per warp → n ≤ 16·9·8 = 1152
+constexpr int F_ACTIVE = 8;             // internal node flag bit (not exported)
+
+struct KP {
+  const double* __restrict__ Z;
+  const double* __restrict__ c;
+  const double* __restrict__ Lt;   // Lᵀ, col-major ld (column i = row i of L)
+  double* beta; double* v; double* bchk;
+  const uint8_t* __restrict__ code;
+  double* U; double* Ub; double* Upart; double* sums; double* sums2;
+  double* nodef;                   // [kBC][4]: lb_best, primal, parent_lb, last dual
+  int* nodei;                      // [kBC][2]: flags, iters
+  unsigned* bar;                   // [2]: count, generation
+  double* out_lb; double* out_primal; int* out_iters; uint8_t* out_flags;
+  int64_t ld, n, n8, p8;
+  int ntiles, nb, check_every, max_iters;
+  double rho, inv_rho, lam0, lam2, M, yy, node_tol;
+  double shrink, sr, a_l1, a_4, psi_l1, psi_4, zsr;
+  bool sr_le_M;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(saddr(b)), "r"(phase) : "memory");
+}
+// TMA bulk copy global → shared (SASS UBLKCP), completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(b))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Grid-wide barrier (sense by generation counter); the kernel is launched cooperatively so
+// all CTAs are co-resident.
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned gen;
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+    __threadfence();
+    unsigned prev = atomicAdd(bar, 1u);
+    if (prev == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
+    } else {
+      unsigned cur;
+      do {
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+      } while (cur == gen);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- the operators
+__device__ __forceinline__ double Tbox(double t, double a, double m) {   // eq:Tdef
+  double at = fabs(t);
+  if (at <= a) return 0.0;
+  if (at <= a + m) return copysign(at - a, t);
+  return copysign(m, t);
+}
+__device__ __forceinline__ double prox(const KP& k, double bt, uint8_t code) {   // eq:minbetalower
+  if (code == 1) return 0.0;
+  double quad = Tbox(k.shrink * bt, 0.0, k.M);
+  if (code == 2) return quad;
+  if (k.sr_le_M) return fabs(bt) >= k.a_l1 + k.sr ? quad : Tbox(bt, k.a_l1, k.M);
+  return Tbox(bt, k.a_4, k.M);
+}
+__device__ __forceinline__ double psi_f(const KP& k, double b, uint8_t code) {   // eq:psi
+  double ab = fabs(b);
+  if (code == 1) return b == 0.0 ? 0.0 : INFINITY;
+  if (ab > k.M) return INFINITY;
+  if (code == 2) return k.lam0 + k.lam2 * b * b;
+  if (k.sr_le_M) return ab >= k.sr ? k.lam0 + k.lam2 * b * b : k.psi_l1 * ab;
+  return k.psi_4 * ab;
+}
+__device__ __forceinline__ double h_f(const KP& k, double x) {                    // eq:hdef
+  return x <= 2.0 * k.M * k.lam2 ? x * x / (4.0 * k.lam2) - k.lam0 : k.M * x - k.lam0 - k.lam2 * k.M * k.M;
+}
+__device__ __forceinline__ double nu_f(const KP& k, double x, uint8_t code) {     // eq:nudef2
+  if (code == 1) return 0.0;
+  if (code == 2) return h_f(k, x);
+  if (k.sr_le_M) return fmax(h_f(k, x), 0.0);
+  return fmax(k.M * x - k.lam0 - k.lam2 * k.M * k.M, 0.0);
+}
+
+// ---------------------------------------------------------------- shared memory layout
+struct Smem {
+  double* Us;      // [kBC][ld]   u of this iteration (node-major)
+  double* tile[2]; // [kPt][ld]   two Z_J buffers
+  double* spart;   // [NW][64]    adjoint partials per warp
+  double* Ws;      // [kBC][12]   w⁺_J (node-major, padded)
+  double* red;     // [kBC][kSums] scratch
+  uint64_t* mbar;  // [3]: tile0, tile1, U
+  int* flags;      // [kBC]
+};
+
+enum { SW_FWD_W = 0, SW_FWD_BETA = 1, SW_FUSED = 2 };
+
+// One sweep over this CTA's tiles.  Forward partials go to Upart[cta]; check sums to sums[cta].
+__device__ void sweep(const KP& k, Smem& s, int mode, bool refresh, bool check, unsigned& phase0,
+                      unsigned& phase1, unsigned& phaseU) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = blockIdx.x, G = gridDim.x;
+  const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
+  const int mt = (int)(k.n8 / 8);            // row tiles of the forward product
+  const int kt = (int)(k.n8 / 4);            // k-steps of the adjoint
+  const int ks0 = kt * warp / NW, ks1 = kt * (warp + 1) / NW;
+  const unsigned tile_bytes = (unsigned)(kPt * k.ld * sizeof(double));
+  const bool fused = (mode == SW_FUSED);
+
+  double acc[MAXMT][2];
+#pragma unroll
+  for (int i = 0; i < MAXMT; i++) acc[i][0] = acc[i][1] = 0.0;
+  // per-thread check sums for (j = tid>>3, node = tid&7), tid < 64
+  double sT1 = 0.0, sT2 = 0.0, sT3 = 0.0, sT4 = 0.0;
+
+  if (fused) {   // u of this iteration → shared memory (written by the previous reduce phase)
+    if (tid == 0) {
+      fence_proxy_async_global();
+      fence_proxy_async_smem();
+      mbar_expect_tx(&s.mbar[2], (unsigned)(kBC * k.ld * sizeof(double)));
+      bulk_g2s(s.Us, k.U, (unsigned)(kBC * k.ld * sizeof(double)), &s.mbar[2]);
+    }
+  }
+  if (tid == 0 && t0 < t1) {
+    fence_proxy_async_smem();
+    mbar_expect_tx(&s.mbar[0], tile_bytes);
+    bulk_g2s(s.tile[0], k.Z + (int64_t)t0 * kPt * k.ld, tile_bytes, &s.mbar[0]);
+  }
+  if (fused) { mbar_wait(&s.mbar[2], phaseU); phaseU ^= 1u; }
+
+  for (int t = t0; t < t1; t++) {
+    const int buf = (t - t0) & 1;
+    // prefetch the next tile into the other buffer (freed by the __syncthreads at the end of t−1)
+    if (tid == 0 && t + 1 < t1) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(&s.mbar[buf ^ 1], tile_bytes);
+      bulk_g2s(s.tile[buf ^ 1], k.Z + (int64_t)(t + 1) * kPt * k.ld, tile_bytes, &s.mbar[buf ^ 1]);
+    }
+    const int64_t col0 = (int64_t)t * kPt;
+    // Issue the state loads for the epilogue before waiting on the tile.
+    double st_beta = 0.0, st_v = 0.0, st_c = 0.0;
+    uint8_t st_code = 1;
+    if (tid < 64) {
+      const int j = tid >> 3, nd = tid & 7;
+      const int64_t e = (col0 + j) * kBC + nd;
+      st_beta = k.beta[e];
+      st_v = k.v[e];
+      st_c = k.c[col0 + j];
+      st_code = k.code[e];
+    }
+    if (buf == 0) { mbar_wait(&s.mbar[0], phase0); phase0 ^= 1u; }
+    else { mbar_wait(&s.mbar[1], phase1); phase1 ^= 1u; }
+    const double* T = s.tile[buf];
+
+    if (fused) {
+      // ---- adjoint: S_J(8 cols × 8 nodes) = Z_Jᵀ U, K = rows split across warps
+      double sc[2] = {0.0, 0.0};
+      for (int q = ks0; q < ks1; q++) {
+        const int r = q * 4 + (lane & 3);
+        double a = T[(lane >> 2) * k.ld + r];          // A[m = col][k = row]
+        double b = s.Us[(lane >> 2) * k.ld + r];       // B[k = row][n = node]
+        dmma(sc, a, b);
+      }
+      // C fragment: row (col j) = lane>>2, cols (node) = 2*(lane&3) + {0,1}
+      s.spart[warp * 64 + (lane >> 2) * 8 + 2 * (lane & 3)] = sc[0];
+      s.spart[warp * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = sc[1];
+      __syncthreads();
+      if (tid < 64) {
+        const int j = tid >> 3, nd = tid & 7;
+        double sv = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) sv += s.spart[w * 64 + j * 8 + nd];   // fixed order
+        double wn = 0.0;
+        if (s.flags[nd] & F_ACTIVE) {
+          const double w = st_c + k.rho * st_beta - st_v;
+          const double b = (w - sv) * k.inv_rho;
+          const double bn = refresh ? st_beta : prox(k, b + st_v * k.inv_rho, st_code);
+          const double vn = st_v + k.rho * (b - bn);
+          if (check) {
+            sT1 = fma(b, sv, sT1);
+            sT2 += nu_f(k, fabs(st_c - sv), st_code);
+            sT3 = fma(st_c, bn, sT3);
+            sT4 += psi_f(k, bn, st_code);
+            k.bchk[(col0 + j) * kBC + nd] = b;
+          }
+          const int64_t e = (col0 + j) * kBC + nd;
+          k.beta[e] = bn;
+          k.v[e] = vn;
+          wn = st_c + k.rho * bn - vn;
+        }
+        s.Ws[nd * 12 + j] = wn;
+      }
+      __syncthreads();
+    } else {
+      if (tid < 64) {
+        const int j = tid >> 3, nd = tid & 7;
+        double wn = 0.0;
+        if (s.flags[nd] & F_ACTIVE)
+          wn = (mode == SW_FWD_BETA) ? st_beta : st_c + k.rho * st_beta - st_v;
+        s.Ws[nd * 12 + j] = wn;
+      }
+      __syncthreads();
+    }
+    // ---- forward: U⁺(rows × 8 nodes) += Z_J (rows × 8 cols) · W_J (8 cols × 8 nodes)
+    {
+      const double b0 = s.Ws[(lane >> 2) * 12 + (lane & 3)];       // B[k = j][n = node]
+      const double b1 = s.Ws[(lane >> 2) * 12 + 4 + (lane & 3)];
+#pragma unroll
+      for (int i = 0; i < MAXMT; i++) {
+        const int m = warp + i * NW;
+        if (m < mt) {
+          const int row = m * 8 + (lane >> 2);
+          double a0 = T[(lane & 3) * k.ld + row];                  // A[m = row][k = col j]
+          double a1 = T[(4 + (lane & 3)) * k.ld + row];
+          dmma(acc[i], a0, b0);
+          dmma(acc[i], a1, b1);
+        }
+      }
+    }
+    __syncthreads();   // tile buffer and Ws free for reuse
+  }
+  // ---- write this CTA's forward partial: Upart[g][node][row]
+  double* up = k.Upart + (int64_t)g * kBC * k.ld;
+#pragma unroll
+  for (int i = 0; i < MAXMT; i++) {
+    const int m = warp + i * NW;
+    if (m < mt) {
+      const int row = m * 8 + (lane >> 2), nd = 2 * (lane & 3);
+      up[(int64_t)nd * k.ld + row] = (t0 < t1) ? acc[i][0] : 0.0;
+      up[(int64_t)(nd + 1) * k.ld + row] = (t0 < t1) ? acc[i][1] : 0.0;
+    }
+  }
+  if (check && fused) {
+    // reduce the 8 column-threads of each node in a fixed order
+    if (tid < 64) {
+      s.spart[tid * 4 + 0] = sT1; s.spart[tid * 4 + 1] = sT2;
+      s.spart[tid * 4 + 2] = sT3; s.spart[tid * 4 + 3] = sT4;
+    }
+    __syncthreads();
+    if (tid < kBC * 4) {
+      const int nd = tid >> 2, q = tid & 3;
+      double a = 0.0;
+      for (int j = 0; j < 8; j++) a += s.spart[(j * 8 + nd) * 4 + q];
+      k.sums[((int64_t)g * kBC + nd) * kSums + q] = a;
+    }
+  }
+}
+
+// Fixed-order grid reduction of the forward partials into dst[node][row] (rows < n8).
+__device__ void reduce_u(const KP& k, double* dst) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x, G = gridDim.x;
+  const int64_t E = (int64_t)kBC * k.n8;
+  const int64_t e0 = E * g / G, e1 = E * (g + 1) / G;
+  for (int64_t e = e0 + warp; e < e1; e += NW) {
+    const int64_t nd = e / k.n8, row = e % k.n8;
+    double a = 0.0;
+    for (int q = lane; q < G; q += 32) a += __ldcg(k.Upart + ((int64_t)q * kBC + nd) * k.ld + row);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) dst[nd * k.ld + row] = a;
+  }
+}
+
+// ‖L (Zβ)‖² partials: rows of L split over CTAs; per node one partial per CTA.
+__device__ void lmatvec_partial(const KP& k, Smem& s) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x, G = gridDim.x;
+  const int64_t i0 = k.n * g / G, i1 = k.n * (g + 1) / G;
+  double part[kBC];
+#pragma unroll
+  for (int nd = 0; nd < kBC; nd++) part[nd] = 0.0;
+  for (int64_t i = i0 + warp; i < i1; i += NW) {
+    double a[kBC];
+#pragma unroll
+    for (int nd = 0; nd < kBC; nd++) a[nd] = 0.0;
+    const double* lrow = k.Lt + i * k.ld;    // row i of L = column i of Lᵀ, entries m ≤ i
+    for (int64_t m = lane; m <= i; m += 32) {
+      const double l = lrow[m];
+#pragma unroll
+      for (int nd = 0; nd < kBC; nd++) a[nd] = fma(l, __ldcg(k.Ub + nd * k.ld + m), a[nd]);
+    }
+#pragma unroll
+    for (int nd = 0; nd < kBC; nd++) {
+      double x = a[nd];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      part[nd] = fma(x, x, part[nd]);
+    }
+  }
+  if (lane == 0)
+    for (int nd = 0; nd < kBC; nd++) s.spart[warp * kBC + nd] = part[nd];
+  __syncthreads();
+  if (threadIdx.x < kBC) {
+    double a = 0.0;
+    for (int w = 0; w < NW; w++) a += s.spart[w * kBC + threadIdx.x];
+    k.sums2[(int64_t)g * kBC + threadIdx.x] = a;
+  }
+}
+
+__global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem s;
+  {
+    double* base = reinterpret_cast<double*>(smem_raw);
+    s.Us = base;
+    s.tile[0] = s.Us + kBC * k.ld;
+    s.tile[1] = s.tile[0] + kPt * k.ld;
+    s.spart = s.tile[1] + kPt * k.ld;
+    s.Ws = s.spart + NW * 64;
+    s.red = s.Ws + kBC * 12;
+    s.mbar = reinterpret_cast<uint64_t*>(s.red + kBC * kSums);
+    s.flags = reinterpret_cast<int*>(s.mbar + 4);
+  }
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&s.mbar[0], 1);
+    mbar_init(&s.mbar[1], 1);
+    mbar_init(&s.mbar[2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < kBC) {
+    s.flags[tid] = __ldcg(k.nodei + tid * 2);
+    s.red[tid] = -INFINITY;
+  }
+  __syncthreads();
+  unsigned ph0 = 0, ph1 = 0, phU = 0;
+
+  // u0 = Z (c + ρβ0 − v0), then the warm/cold refresh sweep (R6)
+  sweep(k, s, SW_FWD_W, false, false, ph0, ph1, phU);
+  grid_sync(k.bar);
+  reduce_u(k, k.U);
+  grid_sync(k.bar);
+  sweep(k, s, SW_FUSED, true, false, ph0, ph1, phU);
+  grid_sync(k.bar);
+  reduce_u(k, k.U);
+  grid_sync(k.bar);
+
+  for (int it = 1; it <= k.max_iters; it++) {
+    const bool chk = (it % k.check_every == 0) || (it == k.max_iters);
+    sweep(k, s, SW_FUSED, false, chk, ph0, ph1, phU);
+    grid_sync(k.bar);
+    reduce_u(k, k.U);
+    grid_sync(k.bar);
+    if (!chk) continue;
+    sweep(k, s, SW_FWD_BETA, false, false, ph0, ph1, phU);
+    grid_sync(k.bar);
+    reduce_u(k, k.Ub);
+    grid_sync(k.bar);
+    lmatvec_partial(k, s);
+    grid_sync(k.bar);
+    // every CTA derives the same per-node decision from the same partials (fixed order)
+    if (tid < kBC) {
+      const int nd = tid;
+      int fl = s.flags[nd];
+      if (fl & F_ACTIVE) {
+        double T1 = 0, T2 = 0, T3 = 0, T4 = 0, T5 = 0;
+        for (int q = 0; q < (int)gridDim.x; q++) {
+          const double* sp = k.sums + ((int64_t)q * kBC + nd) * kSums;
+          T1 += __ldcg(sp + 0); T2 += __ldcg(sp + 1); T3 += __ldcg(sp + 2); T4 += __ldcg(sp + 3);
+          T5 += __ldcg(k.sums2 + (int64_t)q * kBC + nd);
+        }
+        const double dual = 0.5 * k.yy - 0.5 * T1 - T2;
+        const double primal = 0.5 * k.yy - T3 + 0.5 * T5 + T4;
+        const double lbb = fmax(s.red[nd], dual);   // running max of checked duals (R7)
+        s.red[nd] = lbb;
+        bool conv = (primal - lbb) / fmax(1.0, fabs(primal)) <= k.node_tol;
+        if (conv) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_CONVERGED;
+        else if (it == k.max_iters) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_MAXITER;
+        s.flags[nd] = fl;
+        if (blockIdx.x == 0) {
+          k.nodef[nd * 4 + 0] = lbb;
+          k.nodef[nd * 4 + 1] = primal;
+          k.nodef[nd * 4 + 3] = dual;
+          k.nodei[nd * 2 + 0] = fl;
+          k.nodei[nd * 2 + 1] = it;
+        }
+      }
+    }
+    __syncthreads();
+    int any = 0;
+    for (int nd = 0; nd < kBC; nd++) any |= s.flags[nd] & F_ACTIVE;
+    if (!any) break;
+  }
+  if (blockIdx.x == 0 && tid < k.nb) {
+    const int nd = tid;
+    const double lbb = s.red[nd], plb = __ldcg(k.nodef + nd * 4 + 2);
+    k.out_lb[nd] = fmax(lbb, plb);
+    k.out_primal[nd] = k.nodef[nd * 4 + 1];
+    k.out_iters[nd] = k.nodei[nd * 2 + 1];
+    k.out_flags[nd] = (uint8_t)(s.flags[nd] & (L0L2_FLAG_CONVERGED | L0L2_FLAG_MAXITER));
+  }
+}
+
+// ---------------------------------------------------------------- packing / finalize kernels
+
+// code plane and state for one group: column j, node nd (nd ≥ nb and j ≥ p are inactive F0)
+__global__ void pack_kernel(int64_t p, int64_t p8, int nb, uint8_t* code, double* beta, double* v,
+                            const double* const* warm) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p8 * kBC) return;
+  const int64_t j = e / kBC;
+  const int nd = (int)(e % kBC);
+  uint8_t cd = (nd < nb && j < p) ? 0 : 1;
+  code[e] = cd;
+  double b = 0.0, vv = 0.0;
+  if (nd < nb && j < p && warm != nullptr && warm[nd] != nullptr) {
+    b = warm[nd][j];
+    vv = warm[nd][p + j];
+  }
+  beta[e] = b;
+  v[e] = vv;
+}
+
+__global__ void scatter_fix(int nb, const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+                            const uint8_t* __restrict__ val, uint8_t* code, double* beta, int64_t p, int* bad) {
+  const int nd = blockIdx.x;
+  if (nd >= nb) return;
+  for (int64_t q = off[nd] + threadIdx.x; q < off[nd + 1]; q += blockDim.x) {
+    const int32_t j = idx[q];
+    if (j < 0 || j >= p) { atomicOr(bad, 1); continue; }
+    const int64_t e = (int64_t)j * kBC + nd;
+    const uint8_t cd = val[q] ? 2 : 1;
+    const uint8_t old = code[e];
+    if (old != 0 && old != cd) atomicOr(bad, 2);   // F0 ∩ F1 ≠ ∅
+    code[e] = cd;
+    if (cd == 1) beta[e] = 0.0;                    // warm edit: β_j ← 0 on F0
+  }
+}
+
+__global__ void init_nodes(int nb, const double* parent_lb, double* nodef, int* nodei) {
+  const int nd = threadIdx.x;
+  if (nd >= kBC) return;
+  nodef[nd * 4 + 0] = -INFINITY;
+  nodef[nd * 4 + 1] = INFINITY;
+  nodef[nd * 4 + 2] = (nd < nb && parent_lb) ? parent_lb[nd] : -INFINITY;
+  nodef[nd * 4 + 3] = -INFINITY;
+  nodei[nd * 2 + 0] = nd < nb ? F_ACTIVE : 0;
+  nodei[nd * 2 + 1] = 0;
+}
+
+// ẑ, integrality, branch index (R10), support F1 ∪ {ẑ ≥ ½}
+struct BrKey { double frac, ab; int64_t j; };
+__device__ __forceinline__ bool better(const BrKey& a, const BrKey& b) {
+  if (a.frac != b.frac) return a.frac > b.frac;
+  if (a.ab != b.ab) return a.ab > b.ab;
+  return a.j < b.j;
+}
+
+__global__ void __launch_bounds__(512) finalize_kernel(int64_t p, double M, double zsr, bool lam0_pos, double int_tol,
+                                                       const double* __restrict__ beta, const uint8_t* __restrict__ code,
+                                                       double* zhat, int64_t ldz, int32_t* branch_j, uint8_t* flags,
+                                                       int32_t* supp_cnt, int32_t* supp_idx, int64_t supp_stride) {
+  const int nd = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ int wcnt[16];
+  __shared__ int base_s;
+  __shared__ BrKey wkey[16];
+  __shared__ int nonint_s;
+  if (tid == 0) { base_s = 0; nonint_s = 0; }
+  __syncthreads();
+  BrKey best{-1.0, -1.0, (int64_t)1 << 62};
+  int nonint = 0;
+  for (int64_t c0 = 0; c0 < p; c0 += blockDim.x) {
+    const int64_t j = c0 + tid;
+    bool insupp = false;
+    if (j < p) {
+      const double b = beta[j * kBC + nd];
+      const uint8_t cd = code[j * kBC + nd];
+      const double ab = fabs(b);
+      double z;
+      if (cd == 1) z = 0.0;
+      else if (cd == 2) z = 1.0;
+      else z = lam0_pos ? fmin(1.0, fmax(ab / M, zsr * ab)) : (ab > 0.0 ? 1.0 : 0.0);
+      if (zhat) zhat[(int64_t)nd * ldz + j] = z;
+      if (cd == 0) {
+        const double fr = fmin(z, 1.0 - z);
+        if (fr > int_tol) nonint = 1;
+        BrKey kk{fr, ab, j};
+        if (better(kk, best)) best = kk;
+        insupp = z >= 0.5;
+      } else {
+        insupp = (cd == 2);
+      }
+    }
+    // ordered compaction of the support
+    const unsigned m = __ballot_sync(0xffffffffu, insupp);
+    if (lane == 0) wcnt[warp] = __popc(m);
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) { if (w < warp) off += wcnt[w]; tot += wcnt[w]; }
+    if (insupp) {
+      const int pos = base_s + off + __popc(m & ((1u << lane) - 1u));
+      if (pos < supp_stride) supp_idx[(int64_t)nd * supp_stride + pos] = (int32_t)j;
+    }
+    __syncthreads();
+    if (tid == 0) base_s += tot;
+    __syncthreads();
+  }
+  // branch key reduction (warp then block, deterministic comparator)
+  for (int o = 16; o > 0; o >>= 1) {
+    BrKey other{__shfl_xor_sync(0xffffffffu, best.frac, o), __shfl_xor_sync(0xffffffffu, best.ab, o),
+                (int64_t)__shfl_xor_sync(0xffffffffu, (long long)best.j, o)};
+    if (better(other, best)) best = other;
+  }
+  if (lane == 0) wkey[warp] = best;
+  if (nonint) atomicOr(&nonint_s, 1);
+  __syncthreads();
+  if (tid == 0) {
+    BrKey b = wkey[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++) if (better(wkey[w], b)) b = wkey[w];
+    const bool integral = (nonint_s == 0);
+    branch_j[nd] = integral ? -1 : (int32_t)b.j;
+    flags[nd] = (uint8_t)((flags[nd] & ~L0L2_FLAG_INTEGRAL) | (integral ? L0L2_FLAG_INTEGRAL : 0));
+    supp_cnt[nd] = base_s;
+  }
+}
+
+__global__ void unpack_kernel(int64_t p, int nb, const double* __restrict__ beta, const double* __restrict__ v,
+                              double* const* warm) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p * kBC) return;
+  const int64_t j = e / kBC;
+  const int nd = (int)(e % kBC);
+  if (nd >= nb || warm[nd] == nullptr) return;
+  warm[nd][j] = beta[e];
+  warm[nd][p + j] = v[e];
+}
+
+__global__ void fill_y(double* r, int64_t ldr, const double* y, int64_t n, int nb) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * nb) return;
+  r[(e / n) * ldr + e % n] = y[e % n];
+}
+
+}  // namespace
+
+size_t admm_smem_bytes(int64_t ld) {
+  return sizeof(double) * ((size_t)kBC * ld + 2 * (size_t)kPt * ld + NW * 64 + kBC * 12 + kBC * kSums) +
+         4 * sizeof(uint64_t) + kBC * sizeof(int) + 64;
+}
+
+int admm_alloc(Ctx* c) {
+  const int64_t p8 = round8(c->p), ld = c->ld;
+  if (round8(c->n) / 8 > NW * MAXMT) return set_err(c, L0L2_EINVAL, "n = %lld > %d not supported by the fused ADMM kernel", (long long)c->n, NW * MAXMT * 8);
+  const int ntiles = (int)(p8 / kPt);
+  c->grid = std::min(c->sms, ntiles);
+  c->beta = (double*)dalloc(c, sizeof(double) * p8 * kBC);
+  c->v = (double*)dalloc(c, sizeof(double) * p8 * kBC);
+  c->bchk = (double*)dalloc(c, sizeof(double) * p8 * kBC);
+  c->code = (uint8_t*)dalloc(c, p8 * kBC);
+  c->U = (double*)dalloc(c, sizeof(double) * kBC * ld);
+  c->Ub = (double*)dalloc(c, sizeof(double) * kBC * ld);
+  c->Upart = (double*)dalloc(c, sizeof(double) * c->grid * kBC * ld);
+  c->sums = (double*)dalloc(c, sizeof(double) * c->grid * kBC * kSums);
+  c->sums2 = (double*)dalloc(c, sizeof(double) * c->grid * kBC);
+  c->node_f = (double*)dalloc(c, sizeof(double) * kBC * 4);
+  c->node_i = (int*)dalloc(c, sizeof(int) * kBC * 2);
+  c->bar = (unsigned*)dalloc(c, sizeof(unsigned) * 2);
+  c->badflag = (int*)dalloc(c, sizeof(int));
+  if (!c->beta || !c->v || !c->bchk || !c->code || !c->U || !c->Ub || !c->Upart || !c->sums || !c->sums2 ||
+      !c->node_f || !c->node_i || !c->bar || !c->badflag)
+    return set_err(c, L0L2_ENOMEM, "admm work space");
+  L0L2_CUDA(c, cudaMemset(c->U, 0, sizeof(double) * kBC * ld));
+  L0L2_CUDA(c, cudaMemset(c->Ub, 0, sizeof(double) * kBC * ld));
+  L0L2_CUDA(c, cudaMemset(c->Upart, 0, sizeof(double) * c->grid * kBC * ld));
+  L0L2_CUDA(c, cudaMemset(c->bchk, 0, sizeof(double) * p8 * kBC));
+  L0L2_CUDA(c, cudaMemset(c->bar, 0, sizeof(unsigned) * 2));
+  const size_t smem = admm_smem_bytes(ld);
+  L0L2_CUDA(c, cudaFuncSetAttribute(admm_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int nblk = 0;
+  L0L2_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, admm_persistent, kAdmmThreads, smem));
+  if (nblk < 1) return set_err(c, L0L2_EINVAL, "ADMM kernel does not fit an SM (n=%lld)", (long long)c->n);
+  return L0L2_OK;
+}
+
+int pack_group(Ctx* c, int nb, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
+               const double* const* warm_ptrs_dev, cudaStream_t st) {
+  const int64_t p8 = round8(c->p);
+  const int64_t tot = p8 * kBC;
+  pack_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->p, p8, nb, c->code, c->beta, c->v, warm_ptrs_dev);
+  L0L2_LAUNCHED(c);
+  if (fix_off) {
+    L0L2_CUDA(c, cudaMemsetAsync(c->badflag, 0, sizeof(int), st));
+    scatter_fix<<<nb, 128, 0, st>>>(nb, fix_off, fix_idx, fix_val, c->code, c->beta, c->p, c->badflag);
+    L0L2_LAUNCHED(c);
+    int bad = 0;
+    L0L2_CUDA(c, cudaMemcpyAsync(&bad, c->badflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    if (bad & 1) return set_err(c, L0L2_EINVAL, "fixing index out of range");
+    if (bad & 2) return set_err(c, L0L2_EINVAL, "F0 ∩ F1 ≠ ∅ (S:28)");
+  }
+  return L0L2_OK;
+}
+
+int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st) {
+  init_nodes<<<1, 32, 0, st>>>(a.nb, a.parent_lb, c->node_f, c->node_i);
+  L0L2_LAUNCHED(c);
+  KP k{};
+  k.Z = c->Z; k.c = c->c; k.Lt = c->Lt;
+  k.beta = c->beta; k.v = c->v; k.bchk = c->bchk; k.code = c->code;
+  k.U = c->U; k.Ub = c->Ub; k.Upart = c->Upart; k.sums = c->sums; k.sums2 = c->sums2;
+  k.nodef = c->node_f; k.nodei = c->node_i; k.bar = c->bar;
+  k.out_lb = a.lb; k.out_primal = a.primal; k.out_iters = a.iters; k.out_flags = a.flags;
+  k.ld = c->ld; k.n = c->n; k.n8 = round8(c->n); k.p8 = round8(c->p);
+  k.ntiles = (int)(k.p8 / kPt); k.nb = a.nb; k.check_every = c->check_every; k.max_iters = c->max_iters;
+  k.rho = c->rho; k.inv_rho = 1.0 / c->rho; k.lam0 = c->lam0; k.lam2 = c->lam2; k.M = c->M; k.yy = c->yy;
+  k.node_tol = c->node_tol;
+  k.shrink = c->rho / (c->rho + 2.0 * c->lam2);
+  k.sr = std::sqrt(c->lam0 / c->lam2);
+  k.sr_le_M = k.sr <= c->M;
+  k.a_l1 = 2.0 * std::sqrt(c->lam0 * c->lam2) / c->rho;
+  k.a_4 = c->lam0 / (c->M * c->rho) + c->lam2 * c->M / c->rho;
+  k.psi_l1 = 2.0 * std::sqrt(c->lam0 * c->lam2);
+  k.psi_4 = c->lam0 / c->M + c->lam2 * c->M;
+  void* args[] = {&k};
+  L0L2_CUDA(c, cudaLaunchCooperativeKernel((void*)admm_persistent, dim3(c->grid), dim3(kAdmmThreads), args,
+                                           admm_smem_bytes(c->ld), st));
+  L0L2_LAUNCHED(c);
+  return L0L2_OK;
+}
+
+int finalize_group(Ctx* c, int nb, double* zhat, int32_t* branch_j, uint8_t* flags, int32_t* supp_cnt,
+                   int32_t* supp_idx, int64_t supp_stride, cudaStream_t st) {
+  const bool lam0_pos = c->lam0 > 0.0;
+  const double zsr = lam0_pos ? std::sqrt(c->lam2 / c->lam0) : 0.0;
+  finalize_kernel<<<nb, 512, 0, st>>>(c->p, c->M, zsr, lam0_pos, c->int_tol, c->beta, c->code, zhat, c->p,
+                                      branch_j, flags, supp_cnt, supp_idx, supp_stride);
+  L0L2_LAUNCHED(c);
+  return L0L2_OK;
+}
+
+int unpack_warm(Ctx* c, int nb, double* const* warm_ptrs_dev, cudaStream_t st) {
+  const int64_t tot = c->p * kBC;
+  unpack_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->p, nb, c->beta, c->v, warm_ptrs_dev);
+  L0L2_LAUNCHED(c);
+  return L0L2_OK;
+}
+
+int dual_residual(Ctx* c, int nb, double* dual_r, int64_t ldr, cudaStream_t st) {
+  const int64_t tot = c->n * nb;
+  fill_y<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(dual_r, ldr, c->y, c->n, nb);
+  L0L2_LAUNCHED(c);
+  // r̂ = y − X b̂ with b̂ = b at the last check (op(B)(j, node) = bchk[node + j*kBC])
+  return gemm_f64(c, c->n, nb, c->p, -1.0, c->X, c->ld, false, c->bchk, kBC, true, 1.0, dual_r, ldr, st);
+}
+
+}  // namespace l0l2

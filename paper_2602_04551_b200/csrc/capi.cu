@@ -1,0 +1,256 @@
+// C-ABI entry points of include/l0l2.h (argument checking, data placement, batching).
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace l0l2 {
+
+int set_err(Ctx* c, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+void* dalloc(Ctx* c, size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  c->owned.push_back(p);
+  c->bytes += (int64_t)bytes;
+  return p;
+}
+
+namespace {
+
+__global__ void finite_check(const double* __restrict__ X, int64_t ld, int64_t n, int64_t p, int* bad) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * p) return;
+  const double x = X[(e / n) * ld + e % n];
+  if (!isfinite(x)) atomicOr(bad, 1);
+}
+
+}  // namespace
+}  // namespace l0l2
+
+using namespace l0l2;
+
+static thread_local std::string g_last_error;
+
+extern "C" {
+
+void l0l2_default_opts(l0l2_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->M = 0.0;
+  o->rho = 0.0;
+  o->node_tol = 1e-4;
+  o->int_tol = 1e-4;
+  o->check_every = 10;
+  o->max_iters = 10000;
+  o->device = 0;
+  o->x_on_device = 0;
+}
+
+const char* l0l2_last_error(const l0l2_ctx* ctx) {
+  if (ctx) return ctx->impl.err.c_str();
+  return g_last_error.c_str();
+}
+
+void l0l2_destroy(l0l2_ctx* ctx) {
+  if (!ctx) return;
+  Ctx* c = &ctx->impl;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (void* p : c->owned) cudaFree(p);
+  if (c->ub_scratch) cudaFree(c->ub_scratch);
+  for (void* s : c->scr) if (s) cudaFree(s);
+  comm_free(c);
+  delete ctx;
+}
+
+int l0l2_create(const double* X, const double* y, int64_t n, int64_t p, double lambda0, double lambda2,
+                const l0l2_opts* opts, l0l2_ctx** out) {
+  if (out) *out = nullptr;
+  auto fail = [](int code, const char* msg) {
+    g_last_error = msg;
+    return code;
+  };
+  if (!X || !y || !opts || !out) return fail(L0L2_EINVAL, "null argument");
+  if (n <= 0 || p <= 0) return fail(L0L2_EINVAL, "n, p must be > 0");
+  if (!(lambda2 > 0.0) || !std::isfinite(lambda2)) return fail(L0L2_EINVAL, "lambda2 must be > 0 (S:89)");
+  if (!(lambda0 >= 0.0) || !std::isfinite(lambda0)) return fail(L0L2_EINVAL, "lambda0 must be >= 0");
+  if (!(opts->M > 0.0) || !std::isfinite(opts->M)) return fail(L0L2_EINVAL, "M must be > 0");
+  if (!(opts->rho >= 0.0)) return fail(L0L2_EINVAL, "rho must be >= 0");
+  if (opts->check_every < 1 || opts->max_iters < 1) return fail(L0L2_EINVAL, "check_every, max_iters >= 1");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
+    cudaGetLastError();
+    return fail(L0L2_ECUDA, "no CUDA device: this library has no CPU fallback");
+  }
+  if (opts->device < 0 || opts->device >= ndev) return fail(L0L2_EINVAL, "bad device ordinal");
+  l0l2_ctx* ctx = new l0l2_ctx();
+  Ctx* c = &ctx->impl;
+  c->device = opts->device;
+  c->n = n;
+  c->p = p;
+  c->ld = padded_ld(n);
+  c->lam0 = lambda0;
+  c->lam2 = lambda2;
+  c->M = opts->M;
+  c->rho = opts->rho;
+  c->node_tol = opts->node_tol;
+  c->int_tol = opts->int_tol;
+  c->check_every = opts->check_every;
+  c->max_iters = opts->max_iters;
+  int rc = L0L2_OK;
+  auto bail = [&](int code) {
+    g_last_error = c->err;
+    l0l2_destroy(ctx);
+    return code;
+  };
+  if (cudaSetDevice(c->device) != cudaSuccess) return bail(set_err(c, L0L2_ECUDA, "cudaSetDevice"));
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device);
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c->device);
+  if (major < 10) return bail(set_err(c, L0L2_ECUDA, "device is not sm_100 class (built for sm_100a only)"));
+  const int64_t ld = c->ld, p8 = round8(p);
+  c->X = (double*)dalloc(c, sizeof(double) * ld * p8);
+  c->Z = (double*)dalloc(c, sizeof(double) * ld * p8);
+  c->y = (double*)dalloc(c, sizeof(double) * ld);
+  c->c = (double*)dalloc(c, sizeof(double) * p8);
+  c->colsq = (double*)dalloc(c, sizeof(double) * p8);
+  c->L = (double*)dalloc(c, sizeof(double) * ld * n);
+  c->Lt = (double*)dalloc(c, sizeof(double) * ld * n);
+  if (!c->X || !c->Z || !c->y || !c->c || !c->colsq || !c->L || !c->Lt)
+    return bail(set_err(c, L0L2_ENOMEM, "device allocation of problem data (%lld bytes)", (long long)c->bytes));
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return bail(set_err(c, L0L2_ECUDA, "stream"));
+  auto ck = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess) rc = set_err(c, L0L2_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return e == cudaSuccess;
+  };
+  bool ok = ck(cudaMemsetAsync(c->X, 0, sizeof(double) * ld * p8, st), "memset X") &&
+            ck(cudaMemsetAsync(c->y, 0, sizeof(double) * ld, st), "memset y") &&
+            ck(cudaMemsetAsync(c->c, 0, sizeof(double) * p8, st), "memset c") &&
+            ck(cudaMemsetAsync(c->colsq, 0, sizeof(double) * p8, st), "memset colsq");
+  const cudaMemcpyKind kind = opts->x_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  ok = ok && ck(cudaMemcpy2DAsync(c->X, sizeof(double) * ld, X, sizeof(double) * n, sizeof(double) * n, p, kind, st),
+                "copy X") &&
+       ck(cudaMemcpyAsync(c->y, y, sizeof(double) * n, kind, st), "copy y");
+  if (ok) {
+    int* bad = (int*)dalloc(c, sizeof(int));
+    ok = bad && ck(cudaMemsetAsync(bad, 0, sizeof(int), st), "memset");
+    if (ok) {
+      const int64_t tot = n * p;
+      finite_check<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->X, ld, n, p, bad);
+      finite_check<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(c->y, n, n, 1, bad);
+      c->launches += 2;
+      int hb = 0;
+      ok = ck(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st), "copy flag") &&
+           ck(cudaStreamSynchronize(st), "sync");
+      if (ok && hb) {
+        rc = set_err(c, L0L2_EINVAL, "NaN/Inf in X or y");
+        ok = false;
+      }
+    }
+  }
+  if (ok) {
+    rc = precompute(c, st);
+    ok = rc == L0L2_OK;
+  }
+  if (ok) {
+    rc = admm_alloc(c);
+    ok = rc == L0L2_OK;
+  }
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (!ok) return bail(rc ? rc : L0L2_ECUDA);
+  *out = ctx;
+  return L0L2_OK;
+}
+
+int l0l2_info(const l0l2_ctx* ctx, int64_t* n, int64_t* p, double* rho, int64_t* device_bytes, int64_t* launches) {
+  if (!ctx) return L0L2_EINVAL;
+  const Ctx* c = &ctx->impl;
+  if (n) *n = c->n;
+  if (p) *p = c->p;
+  if (rho) *rho = c->rho;
+  if (device_bytes) *device_bytes = c->bytes;
+  if (launches) *launches = c->launches;
+  return L0L2_OK;
+}
+
+int l0l2_bound_batch(l0l2_ctx* ctx, int32_t B, const int64_t* fix_off, const int32_t* fix_idx,
+                     const uint8_t* fix_val, const double* warm_in, const double* parent_lb, double* lb,
+                     double* primal, double* warm_out, double* zhat, double* dual_r, int32_t* branch_j,
+                     int32_t* iters, uint8_t* flags, void* stream) {
+  if (!ctx) return L0L2_EINVAL;
+  Ctx* c = &ctx->impl;
+  if (B < 0) return set_err(c, L0L2_EINVAL, "B < 0");
+  if (B == 0) return L0L2_OK;
+  if (!lb || !primal || !branch_j || !iters || !flags) return set_err(c, L0L2_EINVAL, "null output");
+  if (!fix_off && (fix_idx || fix_val)) return set_err(c, L0L2_EINVAL, "fix_idx without fix_off");
+  L0L2_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t p = c->p;
+  // device scratch: warm pointer table, support compaction (unused here), per-group pointers
+  double** wptr = (double**)c->scratch(sizeof(double*) * 2 * kBC);
+  int32_t* scnt = (int32_t*)c->scratch2(sizeof(int32_t) * kBC + sizeof(int32_t) * kBC * p);
+  if (!wptr || !scnt) return set_err(c, L0L2_ENOMEM, "scratch");
+  int32_t* sidx = scnt + kBC;
+  bool notconv = false;
+  for (int g0 = 0; g0 < B; g0 += kBC) {
+    const int nb = std::min(kBC, B - g0);
+    const double* hin[kBC] = {};
+    double* hout[kBC] = {};
+    for (int k = 0; k < nb; k++) {
+      hin[k] = warm_in ? warm_in + (int64_t)(g0 + k) * 2 * p : nullptr;
+      hout[k] = warm_out ? warm_out + (int64_t)(g0 + k) * 2 * p : nullptr;
+    }
+    L0L2_CUDA(c, cudaMemcpyAsync(wptr, hin, sizeof(hin), cudaMemcpyHostToDevice, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(wptr + kBC, hout, sizeof(hout), cudaMemcpyHostToDevice, st));
+    int rc = pack_group(c, nb, fix_off ? fix_off + g0 : nullptr, fix_idx, fix_val, (const double* const*)wptr, st);
+    if (rc) return rc;
+    BoundArgs a{nb, parent_lb ? parent_lb + g0 : nullptr, lb + g0, primal + g0, iters + g0, flags + g0};
+    rc = run_admm(c, a, st);
+    if (rc) return rc;
+    rc = finalize_group(c, nb, zhat ? zhat + (int64_t)g0 * p : nullptr, branch_j + g0, flags + g0, scnt, sidx, p, st);
+    if (rc) return rc;
+    if (warm_out) {
+      rc = unpack_warm(c, nb, wptr + kBC, st);
+      if (rc) return rc;
+    }
+    if (dual_r) {
+      rc = dual_residual(c, nb, dual_r + (int64_t)g0 * c->n, c->n, st);
+      if (rc) return rc;
+    }
+    uint8_t hf[kBC];
+    L0L2_CUDA(c, cudaMemcpyAsync(hf, flags + g0, nb, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    for (int k = 0; k < nb; k++) notconv |= (hf[k] & L0L2_FLAG_MAXITER) != 0;
+  }
+  return notconv ? L0L2_WNOTCONV : L0L2_OK;
+}
+
+int l0l2_upper_batch(l0l2_ctx* ctx, int32_t B, const int64_t* supp_off, const int32_t* supp_idx, double* obj,
+                     double* beta_s, void* stream) {
+  if (!ctx) return L0L2_EINVAL;
+  Ctx* c = &ctx->impl;
+  if (B < 0 || (B > 0 && (!supp_off || !obj))) return set_err(c, L0L2_EINVAL, "bad arguments");
+  L0L2_CUDA(c, cudaSetDevice(c->device));
+  int rc = upper_batch(c, B, supp_off, supp_idx, obj, beta_s, (cudaStream_t)stream);
+  if (rc) return rc;
+  L0L2_CUDA(c, cudaStreamSynchronize((cudaStream_t)stream));
+  return L0L2_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,136 @@
+// Internal declarations of the l0l2 sm_100a library (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/l0l2.h"
+
+namespace l0l2 {
+
+constexpr int kBC = 8;          // node columns per ADMM pass (DMMA n-dim = 8)
+constexpr int kPt = 8;          // Z columns per tile (DMMA m-dim of the adjoint = 8)
+constexpr int kAdmmThreads = 512;  // 16 warps per persistent CTA
+constexpr int kSums = 6;        // per-node partial sums of a check (see admm.cu)
+
+// leading dimension of Z / X in HBM: ≥ n, even, ≡ 4 (mod 16) doubles so that the 8-byte
+// DMMA fragment loads from a TMA-copied tile are shared-memory bank-conflict free.
+// Also ≥ round8(n), so the DMMA m8 row tiles of the forward product stay inside a column;
+// rows n..ld-1 are zero.
+inline int64_t round8(int64_t n) { return (n + 7) / 8 * 8; }
+inline int64_t padded_ld(int64_t n) {
+  int64_t r8 = round8(n);
+  return r8 + (((4 - r8) % 16) + 16) % 16;
+}
+
+struct Ctx;
+
+struct NcclApi;  // dlopen'ed NCCL entry points (solve.cpp)
+
+struct Ctx {
+  int device = 0;
+  int sms = 148;
+  int64_t n = 0, p = 0, ld = 0;   // ld = padded leading dimension of X and Z
+  double lam0 = 0, lam2 = 0, M = 0, rho = 0;
+  double node_tol = 1e-4, int_tol = 1e-4;
+  int check_every = 10, max_iters = 10000;
+  double yy = 0;                  // ‖y‖²
+  // device data (owned)
+  double *X = nullptr, *Z = nullptr, *y = nullptr, *c = nullptr, *colsq = nullptr, *L = nullptr, *Lt = nullptr;
+  // ADMM work space for one pass of kBC nodes
+  double *beta = nullptr, *v = nullptr, *bchk = nullptr;   // [p][kBC]
+  uint8_t* code = nullptr;                                  // [p][kBC]
+  double *U = nullptr, *Ub = nullptr;                       // [kBC][ld]
+  double *Upart = nullptr;                                  // [grid][kBC][ld]
+  double *sums = nullptr;                                   // [grid][kBC][kSums]
+  double *sums2 = nullptr;                                  // [grid][kBC] ‖L Zβ‖² partials
+  double *node_f = nullptr;                                 // per-node scalars (admm.cu)
+  int *node_i = nullptr;
+  int *badflag = nullptr;
+  unsigned* bar = nullptr;                                  // grid barrier words
+  void* ub_scratch = nullptr;                               // Gram spill for very large supports
+  size_t ub_scratch_bytes = 0;
+  int grid = 0;
+  // scratch for batch I/O in solve (device)
+  std::vector<void*> owned;
+  int64_t bytes = 0;
+  int64_t launches = 0;
+  std::string err;
+  // growable device scratch buffers (batch I/O)
+  void* scr[6] = {};
+  size_t scr_bytes[6] = {};
+  void* scratch_n(int i, size_t b) {
+    if (scr_bytes[i] < b) {
+      if (scr[i]) cudaFree(scr[i]);
+      scr[i] = nullptr;
+      scr_bytes[i] = 0;
+      if (cudaMalloc(&scr[i], b) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+      scr_bytes[i] = b;
+    }
+    return scr[i];
+  }
+  void* scratch(size_t b) { return scratch_n(0, b); }
+  void* scratch2(size_t b) { return scratch_n(1, b); }
+  // multi-GPU
+  int nranks = 1, rank = 0;
+  void* nccl_comm = nullptr;
+  NcclApi* nccl = nullptr;
+  cudaStream_t comm_stream = nullptr;
+};
+
+int set_err(Ctx* c, int code, const char* fmt, ...);
+void* dalloc(Ctx* c, size_t bytes);   // tracked cudaMalloc (nullptr on failure)
+
+#define L0L2_CUDA(ctx, expr)                                                            \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return ::l0l2::set_err((ctx), L0L2_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__,   \
+                             #expr, cudaGetErrorString(e_));                          \
+  } while (0)
+
+#define L0L2_LAUNCHED(ctx)                                                              \
+  do {                                                                                 \
+    (ctx)->launches++;                                                                 \
+    cudaError_t e_ = cudaGetLastError();                                               \
+    if (e_ != cudaSuccess)                                                             \
+      return ::l0l2::set_err((ctx), L0L2_ECUDA, "%s:%d launch: %s", __FILE__, __LINE__, \
+                             cudaGetErrorString(e_));                                 \
+  } while (0)
+
+// ---- launchers (each returns an L0L2 status) -------------------------------------------
+// C (M×N, col-major, ldc) = alpha * op(A) * op(B) + beta * C; op(A) M×K, op(B) K×N.
+// transA: A stored K×M col-major (element (m,k) at A[k + m*lda]); else M×K (A[m + k*lda]).
+// transB: B stored N×K col-major (element (k,n) at B[n + k*ldb]); else K×N (B[k + n*ldb]).
+int gemm_f64(Ctx* c, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+             bool transA, const double* B, int64_t ldb, bool transB, double beta, double* C,
+             int64_t ldc, cudaStream_t st);
+int precompute(Ctx* c, cudaStream_t st);
+int admm_alloc(Ctx* c);
+// bound one group of ≤ kBC nodes whose code plane / warm state are already packed
+struct BoundArgs {
+  int nb;                       // nodes in this group (≤ kBC)
+  const double* parent_lb;      // device [nb] or null
+  double *lb, *primal;          // device [nb]
+  int *iters;                   // device [nb]
+  uint8_t* flags;               // device [nb]
+};
+int pack_group(Ctx* c, int nb, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
+               const double* const* warm_ptrs_dev, cudaStream_t st);
+int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st);
+int finalize_group(Ctx* c, int nb, double* zhat, int32_t* branch_j, uint8_t* flags,
+                   int32_t* supp_cnt, int32_t* supp_idx, int64_t supp_stride, cudaStream_t st);
+int unpack_warm(Ctx* c, int nb, double* const* warm_ptrs_dev, cudaStream_t st);
+int dual_residual(Ctx* c, int nb, double* dual_r, int64_t ldr, cudaStream_t st);
+int upper_batch(Ctx* c, int B, const int64_t* supp_off, const int32_t* supp_idx, double* obj,
+                double* beta_s, cudaStream_t st);
+
+void comm_free(Ctx* c);
+
+}  // namespace l0l2
+
+struct l0l2_ctx {
+  l0l2::Ctx impl;
+};

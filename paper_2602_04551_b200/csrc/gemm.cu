@@ -1,0 +1,119 @@
+// FP64 GEMM on the sm_100a DMMA pipe (mma.sync.m8n8k4.f64 → SASS DMMA.8x8x4).
+// tcgen05 has no f64 kind, so FP64 contractions use warp-level DMMA
+// with register accumulators.  Used by the tree-wide precompute (A = XXᵀ+ρI,
+// blocked Cholesky trailing updates, Z = L⁻¹X) and by the optional r̂ = y − Xb̂ output.
+#include "common.cuh"
+
+namespace l0l2 {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, PADS = 68;  // PADS ≡ 4 (mod 16): conflict-free fragments
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t K, double alpha,
+                                                   const double* __restrict__ A, int64_t lda,
+                                                   const double* __restrict__ B, int64_t ldb,
+                                                   double beta, double* __restrict__ C, int64_t ldc) {
+  __shared__ double As[2][BK][PADS];
+  __shared__ double Bs[2][BK][PADS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 2) * 32;   // 2 warps along m (32 rows each)
+  const int wn = (warp & 3) * 16;    // 4 warps along n (16 cols each)
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  double ra[4], rb[4];
+  auto gload = [&](int64_t k0) {
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      int e = tid + r * 256;              // 0..1023 over the 64×16 tile
+      int mm, kk;
+      if (!TA) { mm = e & 63; kk = e >> 6; } else { kk = e & 15; mm = e >> 4; }
+      int64_t gm = m0 + mm, gk = k0 + kk;
+      double v = 0.0;
+      if (gm < M && gk < K) v = TA ? A[gk + gm * lda] : A[gm + gk * lda];
+      ra[r] = v;
+      int nn;
+      if (!TB) { kk = e & 15; nn = e >> 4; } else { nn = e & 63; kk = e >> 6; }
+      int64_t gn = n0 + nn;
+      gk = k0 + kk;
+      v = 0.0;
+      if (gn < N && gk < K) v = TB ? B[gn + gk * ldb] : B[gk + gn * ldb];
+      rb[r] = v;
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      int e = tid + r * 256;
+      int mm, kk;
+      if (!TA) { mm = e & 63; kk = e >> 6; } else { kk = e & 15; mm = e >> 4; }
+      As[buf][kk][mm] = ra[r];
+      int nn;
+      if (!TB) { kk = e & 15; nn = e >> 4; } else { nn = e & 63; kk = e >> 6; }
+      Bs[buf][kk][nn] = rb[r];
+    }
+  };
+  const int64_t nk = (K + BK - 1) / BK;
+  gload(0);
+  sstore(0);
+  __syncthreads();
+  for (int64_t kt = 0; kt < nk; kt++) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) gload((kt + 1) * BK);
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; i++) af[i] = As[buf][ks + (lane & 3)][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 2; j++) bf[j] = Bs[buf][ks + (lane & 3)][wn + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 2; j++) dmma(acc[i][j], af[i], bf[j]);
+    }
+    if (kt + 1 < nk) sstore(buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        int64_t gm = m0 + wm + i * 8 + (lane >> 2);
+        int64_t gn = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+        if (gm < M && gn < N) {
+          double* cp = C + gm + gn * ldc;
+          *cp = alpha * acc[i][j][h] + (beta == 0.0 ? 0.0 : beta * *cp);
+        }
+      }
+}
+
+}  // namespace
+
+int gemm_f64(Ctx* c, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+             bool transA, const double* B, int64_t ldb, bool transB, double beta, double* C,
+             int64_t ldc, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return L0L2_OK;
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+  if (grid.y > 65535) return set_err(c, L0L2_EINVAL, "gemm: M too large");
+  if (!transA && !transB) gemm_kernel<false, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (!transA && transB) gemm_kernel<false, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (transA && !transB) gemm_kernel<true, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else gemm_kernel<true, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  L0L2_LAUNCHED(c);
+  return L0L2_OK;
+}
+
+}  // namespace l0l2

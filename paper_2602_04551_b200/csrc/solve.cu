@@ -1,0 +1,731 @@
+// Branch-and-bound driver l0l2_solve (Algorithm 1) and the multi-GPU
+// frontier exchange over NCCL.
+//
+// Batched synchronous-round reading of Algorithm 1 (R9, identical to the oracle's
+// bnb_solve so single-GPU trees can be compared node for node):
+//   each round: drop open nodes with LB ≥ UB(1−1e-12); stop when none remain or
+//   (UB − LB)/UB ≤ gap_tol; pop min(B, |N|) nodes by (LB, id);
+//   bound them (l0l2_bound_batch machinery, warm started from the parent state kept in HBM,
+//   P:543); upper bound on the rounded supports; apply every UB improvement of the
+//   round (lowest id wins ties); then in id order prune (LB ≥ UB(1−1e-12) or integral ẑ)
+//   or branch into (F0∪{j}, F1) and (F0, F1∪{j}) with the parent's bound.
+// The node bodies (ADMM, finalize, FPG) run in this library's kernels; the host keeps the
+// priority queue of node descriptors and the refcounted pool of parent warm states (in HBM).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <queue>
+
+#include "common.cuh"
+
+namespace l0l2 {
+
+// ---------------------------------------------------------------- NCCL, loaded at run time
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi* load_nccl(std::string& err) {
+  static NcclApi api;
+  static bool tried = false, ok = false;
+  if (tried) {
+    if (!ok) err = "libnccl.so.2 not loadable";
+    return ok ? &api : nullptr;
+  }
+  tried = true;
+  api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!api.h) {
+    err = std::string("dlopen libnccl.so.2: ") + dlerror();
+    return nullptr;
+  }
+#define SYM(name, f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.h, name)); if (!api.f) { err = name; return nullptr; }
+  SYM("ncclGetUniqueId", GetUniqueId)
+  SYM("ncclCommInitRank", CommInitRank)
+  SYM("ncclAllGather", AllGather)
+  SYM("ncclBroadcast", Broadcast)
+  SYM("ncclSend", Send)
+  SYM("ncclRecv", Recv)
+  SYM("ncclGroupStart", GroupStart)
+  SYM("ncclGroupEnd", GroupEnd)
+  SYM("ncclCommDestroy", CommDestroy)
+  SYM("ncclGetErrorString", GetErrorString)
+#undef SYM
+  ok = true;
+  return &api;
+}
+
+void comm_free(Ctx* c) {
+  if (c->nccl && c->nccl_comm) c->nccl->CommDestroy((ncclComm_t)c->nccl_comm);
+  c->nccl_comm = nullptr;
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  c->comm_stream = nullptr;
+}
+
+#define NCCL_CK(c, expr)                                                                        \
+  do {                                                                                         \
+    ncclResult_t r_ = (expr);                                                                  \
+    if (r_ != ncclSuccess)                                                                     \
+      return set_err((c), L0L2_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #expr,               \
+                     (c)->nccl->GetErrorString(r_));                                           \
+  } while (0)
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+static double secs(Clock::time_point a) { return std::chrono::duration<double>(Clock::now() - a).count(); }
+
+struct Node {
+  double lb;
+  int64_t id;
+  int32_t depth;
+  std::vector<int32_t> fidx;
+  std::vector<uint8_t> fval;
+  int slot;   // warm state slot (−1 = cold)
+};
+struct NodeCmp {   // min-heap by (lb, id)
+  bool operator()(const Node& a, const Node& b) const { return a.lb != b.lb ? a.lb > b.lb : a.id > b.id; }
+};
+
+// Refcounted pool of parent (β, v) states, 2p doubles each, in HBM.
+struct SlotPool {
+  Ctx* c = nullptr;
+  int64_t p = 0;
+  size_t cap = 0;
+  std::vector<double*> chunk;
+  std::vector<int> freel, ref;
+  static constexpr int kPerChunk = 16;
+  double* ptr(int s) const { return chunk[s / kPerChunk] + (int64_t)(s % kPerChunk) * 2 * p; }
+  int alloc() {
+    if (freel.empty()) {
+      if ((chunk.size() + 1) * kPerChunk > cap) return -1;
+      double* m = nullptr;
+      if (cudaMalloc(&m, sizeof(double) * 2 * p * kPerChunk) != cudaSuccess) {
+        cudaGetLastError();
+        cap = chunk.size() * kPerChunk;
+        return -1;
+      }
+      chunk.push_back(m);
+      const int base = (int)ref.size();
+      ref.resize(ref.size() + kPerChunk, 0);
+      for (int i = kPerChunk - 1; i >= 0; i--) freel.push_back(base + i);
+    }
+    const int s = freel.back();
+    freel.pop_back();
+    ref[s] = 1;
+    return s;
+  }
+  void addref(int s) { if (s >= 0) ref[s]++; }
+  void release(int s) {
+    if (s < 0) return;
+    if (--ref[s] == 0) freel.push_back(s);
+  }
+  ~SlotPool() { for (double* m : chunk) cudaFree(m); }
+};
+
+// Per-round device I/O buffers
+struct RoundBufs {
+  int64_t* fix_off = nullptr;
+  int32_t* fix_idx = nullptr;
+  uint8_t* fix_val = nullptr;
+  double* parent_lb = nullptr;
+  double *lb = nullptr, *primal = nullptr, *obj = nullptr, *beta_s = nullptr;
+  int32_t *iters = nullptr, *branch = nullptr, *scnt = nullptr, *sidx = nullptr, *cidx = nullptr;
+  int64_t* soff = nullptr;
+  uint8_t* flags = nullptr;
+  double** wptr = nullptr;
+};
+
+struct Status {   // exchanged every round (8 doubles = 64 B per rank)
+  double ub, lbmin, open, nodes, iters, elapsed, sent, pad;
+};
+
+// Deterministic rebalancing plan from the open counts of all ranks (pure host logic):
+// repeatedly move half the difference from the fullest to the emptiest rank while the emptiest
+// has fewer than B nodes and the difference exceeds 1.  Ties → lowest rank.
+}  // namespace
+
+std::vector<int64_t> rebalance_plan(const std::vector<int64_t>& counts, int64_t B) {
+  std::vector<int64_t> cnt = counts, plan;   // triples (src, dst, k)
+  const int W = (int)cnt.size();
+  for (int guard = 0; guard < 4 * W; guard++) {
+    int hi = 0, lo = 0;
+    for (int r = 1; r < W; r++) {
+      if (cnt[r] > cnt[hi]) hi = r;
+      if (cnt[r] < cnt[lo]) lo = r;
+    }
+    if (cnt[lo] >= B || cnt[hi] - cnt[lo] <= 1) break;
+    int64_t k = (cnt[hi] - cnt[lo]) / 2;
+    if (k <= 0) break;
+    plan.push_back(hi);
+    plan.push_back(lo);
+    plan.push_back(k);
+    cnt[hi] -= k;
+    cnt[lo] += k;
+  }
+  return plan;
+}
+
+namespace {
+
+struct Solver {
+  Ctx* c;
+  l0l2_solve_opts o;
+  cudaStream_t st = nullptr;
+  SlotPool pool;
+  RoundBufs d;
+  std::priority_queue<Node, std::vector<Node>, NodeCmp> open;
+  double UB = 0.0;
+  std::vector<int32_t> inc_S;
+  std::vector<double> inc_b;
+  int64_t next_id = 1, nodes = 0, node_iters = 0, rounds = 0, max_open = 0;
+  double t_bound = 0, t_upper = 0, t_tree = 0, t_comm = 0;
+  bool notconv = false;
+  // multi-rank
+  int W = 1, R = 0;
+  bool partitioned = false;
+  int64_t id_counter = 0, id_base = 0;
+  int ub_owner = 0;
+
+  int64_t new_id() {
+    if (!partitioned) return next_id++;
+    return id_base + (id_counter++) * W + R;
+  }
+
+  int alloc_bufs(int Bmax) {
+    const int64_t p = c->p;
+    auto A = [&](size_t b) { return dalloc(c, b); };
+    d.fix_off = (int64_t*)A(sizeof(int64_t) * (Bmax + 1));
+    d.parent_lb = (double*)A(sizeof(double) * Bmax);
+    d.lb = (double*)A(sizeof(double) * Bmax);
+    d.primal = (double*)A(sizeof(double) * Bmax);
+    d.obj = (double*)A(sizeof(double) * Bmax);
+    d.iters = (int32_t*)A(sizeof(int32_t) * Bmax);
+    d.branch = (int32_t*)A(sizeof(int32_t) * Bmax);
+    d.scnt = (int32_t*)A(sizeof(int32_t) * Bmax);
+    d.sidx = (int32_t*)A(sizeof(int32_t) * (size_t)kBC * p);
+    d.soff = (int64_t*)A(sizeof(int64_t) * (Bmax + 1));
+    d.flags = (uint8_t*)A(Bmax);
+    d.wptr = (double**)A(sizeof(double*) * 2 * kBC);
+    if (!d.fix_off || !d.parent_lb || !d.lb || !d.primal || !d.obj || !d.iters || !d.branch || !d.scnt ||
+        !d.sidx || !d.soff || !d.flags || !d.wptr)
+      return set_err(c, L0L2_ENOMEM, "solve buffers");
+    return L0L2_OK;
+  }
+
+  // Solve one batch of nodes on this GPU; returns results in host vectors.
+  struct Res {
+    double lb, primal, obj;
+    int32_t iters, branch;
+    uint8_t flags;
+    std::vector<int32_t> supp;
+    std::vector<double> beta_s;
+    int slot;
+  };
+
+  int process(std::vector<Node>& batch, std::vector<Res>& res) {
+    const int B = (int)batch.size();
+    res.assign(B, Res{});
+    if (B == 0) return L0L2_OK;
+    auto t0 = Clock::now();
+    const int64_t p = c->p;
+    // fixings (CSR) and parent bounds
+    std::vector<int64_t> off(B + 1, 0);
+    std::vector<int32_t> fidx;
+    std::vector<uint8_t> fval;
+    std::vector<double> plb(B);
+    for (int k = 0; k < B; k++) {
+      fidx.insert(fidx.end(), batch[k].fidx.begin(), batch[k].fidx.end());
+      fval.insert(fval.end(), batch[k].fval.begin(), batch[k].fval.end());
+      off[k + 1] = (int64_t)fidx.size();
+      plb[k] = batch[k].lb;
+    }
+    int32_t* dfi = (int32_t*)c->scratch_n(2, sizeof(int32_t) * std::max<size_t>(1, fidx.size()));
+    uint8_t* dfv = (uint8_t*)c->scratch_n(3, std::max<size_t>(1, fval.size()));
+    if (!dfi || !dfv) return set_err(c, L0L2_ENOMEM, "fix buffers");
+    L0L2_CUDA(c, cudaMemcpyAsync(d.fix_off, off.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
+    if (!fidx.empty()) {
+      L0L2_CUDA(c, cudaMemcpyAsync(dfi, fidx.data(), sizeof(int32_t) * fidx.size(), cudaMemcpyHostToDevice, st));
+      L0L2_CUDA(c, cudaMemcpyAsync(dfv, fval.data(), fval.size(), cudaMemcpyHostToDevice, st));
+    }
+    L0L2_CUDA(c, cudaMemcpyAsync(d.parent_lb, plb.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+    std::vector<int32_t> scnt(B);
+    for (int g0 = 0; g0 < B; g0 += kBC) {
+      const int nb = std::min(kBC, B - g0);
+      double* hp[2 * kBC] = {};
+      for (int k = 0; k < nb; k++) {
+        const Node& u = batch[g0 + k];
+        hp[k] = u.slot >= 0 ? pool.ptr(u.slot) : nullptr;
+        const int s = pool.alloc();
+        res[g0 + k].slot = s;
+        hp[kBC + k] = s >= 0 ? pool.ptr(s) : nullptr;
+      }
+      L0L2_CUDA(c, cudaMemcpyAsync(d.wptr, hp, sizeof(hp), cudaMemcpyHostToDevice, st));
+      int rc = pack_group(c, nb, d.fix_off + g0, dfi, dfv, (const double* const*)d.wptr, st);
+      if (rc) return rc;
+      BoundArgs a{nb, d.parent_lb + g0, d.lb + g0, d.primal + g0, d.iters + g0, d.flags + g0};
+      if ((rc = run_admm(c, a, st))) return rc;
+      if ((rc = finalize_group(c, nb, nullptr, d.branch + g0, d.flags + g0, d.scnt + g0, d.sidx, p, st))) return rc;
+      if ((rc = unpack_warm(c, nb, d.wptr + kBC, st))) return rc;
+      // supports of this group → host (counts first)
+      L0L2_CUDA(c, cudaMemcpyAsync(scnt.data() + g0, d.scnt + g0, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+      L0L2_CUDA(c, cudaStreamSynchronize(st));
+      for (int k = 0; k < nb; k++) {
+        res[g0 + k].supp.resize(scnt[g0 + k]);
+        if (scnt[g0 + k] > 0)
+          L0L2_CUDA(c, cudaMemcpyAsync(res[g0 + k].supp.data(), d.sidx + (int64_t)k * p, sizeof(int32_t) * scnt[g0 + k],
+                                       cudaMemcpyDeviceToHost, st));
+      }
+    }
+    std::vector<double> hlb(B), hpr(B);
+    std::vector<int32_t> hit(B), hbr(B);
+    std::vector<uint8_t> hfl(B);
+    L0L2_CUDA(c, cudaMemcpyAsync(hlb.data(), d.lb, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(hpr.data(), d.primal, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(hit.data(), d.iters, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(hbr.data(), d.branch, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(hfl.data(), d.flags, B, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    // the parents' warm states have been consumed by pack_group
+    for (int k = 0; k < B; k++) pool.release(batch[k].slot);
+    t_bound += secs(t0);
+    // ---- upper bounds on the rounded supports
+    auto t1 = Clock::now();
+    std::vector<int64_t> so(B + 1, 0);
+    std::vector<int32_t> sall;
+    for (int k = 0; k < B; k++) {
+      sall.insert(sall.end(), res[k].supp.begin(), res[k].supp.end());
+      so[k + 1] = (int64_t)sall.size();
+    }
+    int32_t* dsi = (int32_t*)c->scratch_n(4, sizeof(int32_t) * std::max<size_t>(1, sall.size()));
+    double* dbs = (double*)c->scratch_n(5, sizeof(double) * std::max<size_t>(1, sall.size()));
+    if (!dsi || !dbs) return set_err(c, L0L2_ENOMEM, "support buffers");
+    L0L2_CUDA(c, cudaMemcpyAsync(d.soff, so.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
+    if (!sall.empty())
+      L0L2_CUDA(c, cudaMemcpyAsync(dsi, sall.data(), sizeof(int32_t) * sall.size(), cudaMemcpyHostToDevice, st));
+    int rc = upper_batch(c, B, d.soff, dsi, d.obj, dbs, st);
+    if (rc) return rc;
+    std::vector<double> hob(B), hbs(sall.size());
+    L0L2_CUDA(c, cudaMemcpyAsync(hob.data(), d.obj, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+    if (!sall.empty())
+      L0L2_CUDA(c, cudaMemcpyAsync(hbs.data(), dbs, sizeof(double) * sall.size(), cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    for (int k = 0; k < B; k++) {
+      Res& r = res[k];
+      r.lb = hlb[k];
+      r.primal = hpr[k];
+      r.iters = hit[k];
+      r.branch = hbr[k];
+      r.flags = hfl[k];
+      r.obj = hob[k];
+      r.beta_s.assign(hbs.begin() + so[k], hbs.begin() + so[k + 1]);
+      if (r.flags & L0L2_FLAG_MAXITER) notconv = true;
+      nodes++;
+      node_iters += r.iters;
+    }
+    t_upper += secs(t1);
+    return L0L2_OK;
+  }
+
+  // Algorithm 1 body for one solved batch (id order; UB first, then prune/branch)
+  void update_tree(std::vector<Node>& batch, std::vector<Res>& res) {
+    const int B = (int)batch.size();
+    std::vector<int> order(B);
+    for (int k = 0; k < B; k++) order[k] = k;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return batch[a].id < batch[b].id; });
+    for (int k : order)
+      if (res[k].obj < UB) {
+        UB = res[k].obj;
+        inc_S = res[k].supp;
+        inc_b = res[k].beta_s;
+        ub_owner = R;
+      }
+    for (int k : order) {
+      Res& r = res[k];
+      const bool integral = (r.flags & L0L2_FLAG_INTEGRAL) != 0;
+      const bool pruned = r.lb >= UB * (1.0 - 1e-12) || integral || r.branch < 0;
+      if (pruned) {
+        pool.release(r.slot);
+        continue;
+      }
+      const Node& u = batch[k];
+      Node a{r.lb, 0, u.depth + 1, u.fidx, u.fval, r.slot};
+      Node b{r.lb, 0, u.depth + 1, u.fidx, u.fval, r.slot};
+      a.fidx.push_back(r.branch);
+      a.fval.push_back(0);   // F0 ∪ {j}
+      b.fidx.push_back(r.branch);
+      b.fval.push_back(1);   // F1 ∪ {j}
+      a.id = new_id();
+      b.id = new_id();
+      pool.addref(r.slot);   // two children share the parent's state (ref 1 → 2)
+      open.push(std::move(a));
+      open.push(std::move(b));
+    }
+    max_open = std::max<int64_t>(max_open, (int64_t)open.size());
+  }
+
+  void prune_open() {
+    std::vector<Node> keep;
+    keep.reserve(open.size());
+    while (!open.empty()) {
+      Node u = open.top();
+      open.pop();
+      if (u.lb >= UB * (1.0 - 1e-12)) pool.release(u.slot);
+      else keep.push_back(std::move(u));
+    }
+    for (auto& u : keep) open.push(std::move(u));
+  }
+
+  double local_lbmin() const { return open.empty() ? INFINITY : open.top().lb; }
+
+  // ---- multi-rank helpers
+  int allgather_status(const Status& mine, std::vector<Status>& all) {
+    auto t0 = Clock::now();
+    double* dbuf = (double*)c->scratch_n(2, sizeof(double) * 8 * (W + 1));
+    if (!dbuf) return set_err(c, L0L2_ENOMEM, "status buffer");
+    L0L2_CUDA(c, cudaMemcpyAsync(dbuf, &mine, sizeof(Status), cudaMemcpyHostToDevice, st));
+    NCCL_CK(c, c->nccl->AllGather(dbuf, dbuf + 8, 8, ncclFloat64, (ncclComm_t)c->nccl_comm, st));
+    all.resize(W);
+    L0L2_CUDA(c, cudaMemcpyAsync(all.data(), dbuf + 8, sizeof(Status) * W, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    t_comm += secs(t0);
+    return L0L2_OK;
+  }
+
+  // send k nodes (odd positions of the local best-first order first) from src to dst
+  int rebalance(const std::vector<int64_t>& plan) {
+    auto t0 = Clock::now();
+    const int64_t p = c->p;
+    for (size_t q = 0; q + 2 < plan.size(); q += 3) {
+      const int src = (int)plan[q], dst = (int)plan[q + 1];
+      const int64_t k = plan[q + 2];
+      if (R != src && R != dst) continue;
+      const int peer = (R == src) ? dst : src;
+      // meta: per node [lb, id, depth, nfix, has_warm]
+      std::vector<double> meta(5 * k, 0.0);
+      std::vector<int32_t> fix;
+      std::vector<Node> out;
+      if (R == src) {
+        std::vector<Node> all;
+        while (!open.empty()) { all.push_back(open.top()); open.pop(); }
+        std::vector<Node> keep;
+        for (size_t i = 0; i < all.size(); i++) {
+          if ((int64_t)out.size() < k && (i % 2 == 1 || (int64_t)(all.size() - i) <= k - (int64_t)out.size()))
+            out.push_back(std::move(all[i]));
+          else
+            keep.push_back(std::move(all[i]));
+        }
+        for (auto& u : keep) open.push(std::move(u));
+        for (int64_t i = 0; i < k; i++) {
+          const Node& u = out[i];
+          meta[5 * i + 0] = u.lb;
+          meta[5 * i + 1] = (double)u.id;
+          meta[5 * i + 2] = u.depth;
+          meta[5 * i + 3] = (double)u.fidx.size();
+          meta[5 * i + 4] = u.slot >= 0 ? 1.0 : 0.0;
+          for (size_t f = 0; f < u.fidx.size(); f++) fix.push_back(u.fidx[f] * 2 + u.fval[f]);
+        }
+      }
+      double* dmeta = (double*)c->scratch_n(2, sizeof(double) * std::max<int64_t>(8, 5 * k));
+      if (!dmeta) return set_err(c, L0L2_ENOMEM, "rebalance buffers");
+      if (R == src) L0L2_CUDA(c, cudaMemcpyAsync(dmeta, meta.data(), sizeof(double) * 5 * k, cudaMemcpyHostToDevice, st));
+      NCCL_CK(c, c->nccl->GroupStart());
+      if (R == src) NCCL_CK(c, c->nccl->Send(dmeta, 5 * k, ncclFloat64, peer, (ncclComm_t)c->nccl_comm, st));
+      else NCCL_CK(c, c->nccl->Recv(dmeta, 5 * k, ncclFloat64, peer, (ncclComm_t)c->nccl_comm, st));
+      NCCL_CK(c, c->nccl->GroupEnd());
+      if (R == dst) {
+        L0L2_CUDA(c, cudaMemcpyAsync(meta.data(), dmeta, sizeof(double) * 5 * k, cudaMemcpyDeviceToHost, st));
+        L0L2_CUDA(c, cudaStreamSynchronize(st));
+      }
+      int64_t nfix = 0;
+      for (int64_t i = 0; i < k; i++) nfix += (int64_t)meta[5 * i + 3];
+      // fixings and warm states in one device buffer: [nfix int32 padded to doubles][k × 2p]
+      const int64_t fix_d = (nfix + 1) / 2;
+      double* dpay = (double*)c->scratch_n(3, sizeof(double) * std::max<int64_t>(1, fix_d + k * 2 * p));
+      if (!dpay) return set_err(c, L0L2_ENOMEM, "rebalance payload");
+      if (R == src) {
+        if (nfix) L0L2_CUDA(c, cudaMemcpyAsync(dpay, fix.data(), sizeof(int32_t) * nfix, cudaMemcpyHostToDevice, st));
+        for (int64_t i = 0; i < k; i++) {
+          double* dstp = dpay + fix_d + i * 2 * p;
+          if (out[i].slot >= 0)
+            L0L2_CUDA(c, cudaMemcpyAsync(dstp, pool.ptr(out[i].slot), sizeof(double) * 2 * p, cudaMemcpyDeviceToDevice, st));
+          else
+            L0L2_CUDA(c, cudaMemsetAsync(dstp, 0, sizeof(double) * 2 * p, st));
+        }
+      }
+      NCCL_CK(c, c->nccl->GroupStart());
+      if (R == src) NCCL_CK(c, c->nccl->Send(dpay, fix_d + k * 2 * p, ncclFloat64, peer, (ncclComm_t)c->nccl_comm, st));
+      else NCCL_CK(c, c->nccl->Recv(dpay, fix_d + k * 2 * p, ncclFloat64, peer, (ncclComm_t)c->nccl_comm, st));
+      NCCL_CK(c, c->nccl->GroupEnd());
+      if (R == src) {
+        L0L2_CUDA(c, cudaStreamSynchronize(st));
+        for (auto& u : out) pool.release(u.slot);
+      } else {
+        std::vector<int32_t> hf(nfix);
+        if (nfix) L0L2_CUDA(c, cudaMemcpyAsync(hf.data(), dpay, sizeof(int32_t) * nfix, cudaMemcpyDeviceToHost, st));
+        L0L2_CUDA(c, cudaStreamSynchronize(st));
+        int64_t f = 0;
+        for (int64_t i = 0; i < k; i++) {
+          Node u;
+          u.lb = meta[5 * i + 0];
+          u.id = (int64_t)meta[5 * i + 1];
+          u.depth = (int32_t)meta[5 * i + 2];
+          const int64_t nf = (int64_t)meta[5 * i + 3];
+          for (int64_t q2 = 0; q2 < nf; q2++, f++) {
+            u.fidx.push_back(hf[f] >> 1);
+            u.fval.push_back((uint8_t)(hf[f] & 1));
+          }
+          u.slot = -1;
+          if (meta[5 * i + 4] != 0.0) {
+            u.slot = pool.alloc();
+            if (u.slot >= 0)
+              L0L2_CUDA(c, cudaMemcpyAsync(pool.ptr(u.slot), dpay + fix_d + i * 2 * p, sizeof(double) * 2 * p,
+                                           cudaMemcpyDeviceToDevice, st));
+          }
+          open.push(std::move(u));
+        }
+        L0L2_CUDA(c, cudaStreamSynchronize(st));
+      }
+    }
+    t_comm += secs(t0);
+    return L0L2_OK;
+  }
+
+  void partition() {
+    std::vector<Node> all;
+    while (!open.empty()) { all.push_back(open.top()); open.pop(); }
+    for (size_t i = 0; i < all.size(); i++) {
+      if ((int)(i % W) == R) open.push(std::move(all[i]));
+      else pool.release(all[i].slot);
+    }
+    partitioned = true;
+    id_base = next_id;
+  }
+};
+
+}  // namespace
+}  // namespace l0l2
+
+using namespace l0l2;
+
+extern "C" {
+
+void l0l2_default_solve_opts(l0l2_solve_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->gap_tol = 1e-2;
+  o->time_limit_s = 0.0;
+  o->node_limit = 0;
+  o->batch = 16;
+  o->rebalance_every = 8;
+  o->warm_bytes_cap = 0;
+  o->verbose = 0;
+}
+
+int l0l2_nccl_unique_id(uint8_t out[128]) {
+  std::string err;
+  NcclApi* api = load_nccl(err);
+  if (!api) return L0L2_ENCCL;
+  ncclUniqueId id;
+  if (api->GetUniqueId(&id) != ncclSuccess) return L0L2_ENCCL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out, &id, 128);
+  return L0L2_OK;
+}
+
+int l0l2_comm_init(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id[128]) {
+  if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) return L0L2_EINVAL;
+  Ctx* c = &ctx->impl;
+  if (nranks == 1) {
+    c->nranks = 1;
+    c->rank = 0;
+    return L0L2_OK;
+  }
+  std::string err;
+  c->nccl = load_nccl(err);
+  if (!c->nccl) return set_err(c, L0L2_ENCCL, "%s", err.c_str());
+  L0L2_CUDA(c, cudaSetDevice(c->device));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  ncclComm_t comm;
+  NCCL_CK(c, c->nccl->CommInitRank(&comm, nranks, uid, rank));
+  c->nccl_comm = comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  return L0L2_OK;
+}
+
+int l0l2_rebalance_plan(int32_t nranks, const int64_t* counts, int64_t batch, int64_t* plan, int32_t max_moves) {
+  if (nranks < 1 || !counts || !plan) return -1;
+  std::vector<int64_t> cnt(counts, counts + nranks);
+  std::vector<int64_t> pl = rebalance_plan(cnt, batch);
+  const int moves = (int)(pl.size() / 3);
+  for (int i = 0; i < std::min(moves, (int)max_moves) * 3; i++) plan[i] = pl[i];
+  return moves;
+}
+
+int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, double* obj, double* gap,
+               l0l2_stats* stats) {
+  if (!ctx || !beta) return L0L2_EINVAL;
+  Ctx* c = &ctx->impl;
+  l0l2_solve_opts o;
+  if (opts_in) o = *opts_in;
+  else l0l2_default_solve_opts(&o);
+  if (o.batch < 1) return set_err(c, L0L2_EINVAL, "batch < 1");
+  L0L2_CUDA(c, cudaSetDevice(c->device));
+  const auto T0 = Clock::now();
+  Solver S{};
+  S.c = c;
+  S.o = o;
+  S.W = c->nranks;
+  S.R = c->rank;
+  if (S.W > 1 && !c->nccl_comm) return set_err(c, L0L2_ENCCL, "communicator not initialised");
+  L0L2_CUDA(c, cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking));
+  struct StreamGuard { cudaStream_t s; ~StreamGuard() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } } sg{S.st};
+  S.pool.c = c;
+  S.pool.p = c->p;
+  {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    size_t capb = o.warm_bytes_cap > 0 ? (size_t)o.warm_bytes_cap : fr / 4;
+    S.pool.cap = std::max<size_t>(SlotPool::kPerChunk, capb / (sizeof(double) * 2 * c->p));
+  }
+  int rc = S.alloc_bufs(o.batch);
+  if (rc) return rc;
+  S.UB = 0.5 * c->yy;   // β = 0 is feasible
+  S.open.push(Node{-INFINITY, 0, 0, {}, {}, -1});
+  double LB = -INFINITY;
+  int status = 0;
+  std::vector<Status> all;
+  while (true) {
+    auto tt = Clock::now();
+    S.prune_open();
+    S.t_tree += secs(tt);
+    double gUB = S.UB, gLB;
+    int64_t gopen = (int64_t)S.open.size(), gnodes = S.nodes;
+    double elapsed = secs(T0);
+    if (S.W > 1) {
+      Status mine{S.UB, S.local_lbmin(), (double)S.open.size(), (double)S.nodes, (double)S.node_iters, elapsed, 0, 0};
+      if ((rc = S.allgather_status(mine, all))) return rc;
+      gopen = 0;
+      gnodes = 0;
+      gLB = INFINITY;
+      int owner = 0;
+      for (int r = 0; r < S.W; r++) {
+        if (all[r].ub < gUB || (all[r].ub == gUB && r < owner)) { gUB = all[r].ub; owner = r; }
+        gLB = std::min(gLB, all[r].lbmin);
+        gopen += (int64_t)all[r].open;
+        gnodes += (int64_t)all[r].nodes;
+        elapsed = std::max(elapsed, all[r].elapsed);
+      }
+      // owner = lowest rank holding the global UB
+      for (int r = 0; r < S.W; r++) if (all[r].ub == gUB) { owner = r; break; }
+      S.ub_owner = owner;
+      if (gUB < S.UB) {
+        S.UB = gUB;   // incumbent vector stays with its owner until the end
+        S.prune_open();
+      }
+    } else {
+      gLB = S.local_lbmin();
+    }
+    if (gopen == 0) { LB = gUB; status = 0; break; }
+    LB = gLB;
+    if (gUB > 0 && (gUB - LB) / gUB <= o.gap_tol) { status = 1; break; }
+    if (o.node_limit > 0 && gnodes >= o.node_limit) { status = 2; break; }
+    if (o.time_limit_s > 0 && elapsed >= o.time_limit_s) { status = 3; break; }
+    if (S.W > 1) {
+      if (!S.partitioned) {
+        if (gopen >= S.W) S.partition();   // every rank holds the same tree until here
+      } else if (o.rebalance_every > 0 && S.rounds % o.rebalance_every == 0) {
+        std::vector<int64_t> cnt(S.W);
+        for (int r = 0; r < S.W; r++) cnt[r] = (int64_t)all[r].open;
+        std::vector<int64_t> plan = rebalance_plan(cnt, o.batch);
+        if (!plan.empty() && (rc = S.rebalance(plan))) return rc;
+      }
+    }
+    std::vector<Node> batch;
+    while (!S.open.empty() && (int)batch.size() < o.batch) {
+      batch.push_back(S.open.top());
+      S.open.pop();
+    }
+    S.rounds++;
+    std::vector<Solver::Res> res;
+    if ((rc = S.process(batch, res))) return rc;
+    tt = Clock::now();
+    S.update_tree(batch, res);
+    S.t_tree += secs(tt);
+    if (o.verbose && S.R == 0)
+      fprintf(stderr, "[l0l2] round %lld nodes %lld open %zu UB %.10g LB %.10g gap %.3e\n", (long long)S.rounds,
+              (long long)S.nodes, S.open.size(), S.UB, LB, gUB > 0 ? (gUB - LB) / gUB : 0.0);
+  }
+  // final incumbent → every rank
+  const int64_t p = c->p;
+  std::vector<double> hb(p, 0.0);
+  for (size_t i = 0; i < S.inc_S.size(); i++) hb[S.inc_S[i]] = S.inc_b[i];
+  double final_ub = S.UB;
+  if (S.W > 1) {
+    auto t0 = Clock::now();
+    double* db = (double*)c->scratch_n(3, sizeof(double) * (p + 1));
+    if (!db) return set_err(c, L0L2_ENOMEM, "beta buffer");
+    hb.push_back(S.UB);
+    L0L2_CUDA(c, cudaMemcpyAsync(db, hb.data(), sizeof(double) * (p + 1), cudaMemcpyHostToDevice, S.st));
+    NCCL_CK(c, c->nccl->Broadcast(db, db, p + 1, ncclFloat64, S.ub_owner, (ncclComm_t)c->nccl_comm, S.st));
+    L0L2_CUDA(c, cudaMemcpyAsync(hb.data(), db, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost, S.st));
+    L0L2_CUDA(c, cudaStreamSynchronize(S.st));
+    final_ub = hb[p];
+    Status mine{S.UB, 0, 0, (double)S.nodes, (double)S.node_iters, 0, 0, 0};
+    if ((rc = S.allgather_status(mine, all))) return rc;
+    S.t_comm += secs(t0);
+  }
+  std::memcpy(beta, hb.data(), sizeof(double) * p);
+  const double g = final_ub > 0 ? std::max(0.0, (final_ub - LB) / final_ub) : 0.0;
+  if (obj) *obj = final_ub;
+  if (gap) *gap = g;
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->nodes = S.nodes;
+    stats->node_iters = S.node_iters;
+    stats->rounds = S.rounds;
+    stats->max_open = S.max_open;
+    stats->nodes_global = S.nodes;
+    stats->node_iters_global = S.node_iters;
+    if (S.W > 1) {
+      stats->nodes_global = 0;
+      stats->node_iters_global = 0;
+      for (int r = 0; r < S.W; r++) {
+        stats->nodes_global += (int64_t)all[r].nodes;
+        stats->node_iters_global += (int64_t)all[r].iters;
+      }
+    }
+    stats->t_total = secs(T0);
+    stats->t_bound = S.t_bound;
+    stats->t_upper = S.t_upper;
+    stats->t_tree = S.t_tree;
+    stats->t_comm = S.t_comm;
+    stats->lb = LB;
+    stats->ub = final_ub;
+    stats->gap = g;
+    stats->status = status;
+    int64_t ss = 0;
+    for (int64_t j = 0; j < p; j++) ss += beta[j] != 0.0;
+    stats->support_size = (int32_t)ss;
+  }
+  if (status >= 2) return L0L2_WLIMIT;
+  return S.notconv ? L0L2_WNOTCONV : L0L2_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,200 @@
+// Batched upper bound on candidate supports (§3.3-§3.4).
+//
+// For each support S (one warp per support) minimise eq:upperboundbeta
+//     U_S(β) = ½‖y − X_Sβ‖² + λ2‖β‖²   s.t. |β_i| ≤ M
+// by the paper's fast proximal gradient method: Nesterov extrapolation t/(t+3)
+// (eq:fpg_extrapolate), gradient (eq:fpg_grad), box projection (eq:fpg_step) and Armijo
+// backtracking (eq:fpg_armijo).  B200 form: the Gram matrix
+// Q = X_SᵀX_S + 2λ2I and q = X_Sᵀy = c_S are formed once per support in shared memory, so each
+// iteration works in s-space:  ∇ = Qβ̃ − q,  U_S(β) = ½‖y‖² − qᵀβ + ½βᵀQβ.  These are the same
+// iterates as the paper's masked dense form in exact arithmetic.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace l0l2 {
+namespace {
+
+constexpr int kRC = 32;   // rows of X_S staged per Gram chunk
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ double warp_max(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+// one warp (one CTA) per support
+__global__ void __launch_bounds__(32) fpg_kernel(const double* __restrict__ X, int64_t ld, int64_t n,
+                                                 const double* __restrict__ y, const double* __restrict__ c,
+                                                 double yy, double lam0, double lam2, double M,
+                                                 const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+                                                 double* __restrict__ obj, double* __restrict__ beta_s,
+                                                 double* __restrict__ Qglobal, int64_t qstride, int smax_smem,
+                                                 int max_iters) {
+  extern __shared__ double sm[];
+  const int nd = blockIdx.x, lane = threadIdx.x;
+  const int64_t o0 = off[nd];
+  const int s = (int)(off[nd + 1] - o0);
+  if (s == 0) {
+    if (lane == 0) obj[nd] = 0.5 * yy;
+    return;
+  }
+  const int32_t* S = idx + o0;
+  double* Q = (s <= smax_smem) ? sm : Qglobal + (int64_t)nd * qstride;
+  double* vec = (s <= smax_smem) ? sm + (int64_t)s * s : sm;      // 6 vectors of length s
+  double* q = vec;
+  double* bb = vec + s;       // β^t
+  double* bp = vec + 2 * s;   // β^{t−1}
+  double* bt = vec + 3 * s;   // β̃
+  double* g = vec + 4 * s;    // ∇
+  double* bn = vec + 5 * s;   // trial β^{t+1}
+  double* Xc = vec + 6 * s;   // [kRC][s] staging of X_S rows
+
+  // ---- Gram Q = X_SᵀX_S + 2λ2 I, staged kRC rows at a time (fixed summation order)
+  for (int e = lane; e < s * s; e += 32) Q[e] = 0.0;
+  __syncwarp();
+  for (int64_t r0 = 0; r0 < n; r0 += kRC) {
+    const int rr = (int)((n - r0) < kRC ? (n - r0) : kRC);
+    for (int e = lane; e < rr * s; e += 32) {
+      const int a = e / rr, r = e % rr;
+      Xc[r * s + a] = X[(int64_t)S[a] * ld + r0 + r];
+    }
+    __syncwarp();
+    for (int e = lane; e < s * s; e += 32) {
+      const int a = e / s, b = e % s;
+      if (b < a) continue;
+      double acc = Q[a * s + b];
+      for (int r = 0; r < rr; r++) acc = fma(Xc[r * s + a], Xc[r * s + b], acc);
+      Q[a * s + b] = acc;
+    }
+    __syncwarp();
+  }
+  for (int e = lane; e < s * s; e += 32) {
+    const int a = e / s, b = e % s;
+    if (b < a) Q[a * s + b] = Q[b * s + a];
+    else if (a == b) Q[a * s + b] += 2.0 * lam2;
+  }
+  for (int a = lane; a < s; a += 32) { q[a] = c[S[a]]; bb[a] = 0.0; bp[a] = 0.0; }
+  __syncwarp();
+  // Gershgorin bound on λmax(Q) → initial step α0 = 1/L̂ (R12)
+  double Lh = 0.0;
+  for (int a = lane; a < s; a += 32) {
+    double r = 0.0;
+    for (int b = 0; b < s; b++) r += fabs(Q[a * s + b]);
+    Lh = fmax(Lh, r);
+  }
+  Lh = warp_max(Lh);
+  const double alpha0 = 1.0 / Lh;
+
+  double f_cur = 0.0;   // f(β) = −qᵀβ + ½βᵀQβ  (U_S = ½‖y‖² + f)
+  for (int t = 0; t < max_iters; t++) {
+    const double mom = (double)t / (double)(t + 3);
+    for (int a = lane; a < s; a += 32) bt[a] = bb[a] + mom * (bb[a] - bp[a]);
+    __syncwarp();
+    double qb = 0.0, bg = 0.0;
+    for (int a = lane; a < s; a += 32) {
+      double r = 0.0;
+      for (int b = 0; b < s; b++) r = fma(Q[a * s + b], bt[b], r);
+      const double ga = r - q[a];
+      g[a] = ga;
+      qb = fma(q[a], bt[a], qb);
+      bg = fma(bt[a], ga, bg);
+    }
+    __syncwarp();
+    qb = warp_sum(qb);
+    bg = warp_sum(bg);
+    const double f_t = 0.5 * bg - 0.5 * qb;     // ½β̃ᵀ(Qβ̃ − q) − ½qᵀβ̃
+    double alpha = alpha0, f_n = 0.0;
+    for (int ls = 0; ls < 60; ls++) {
+      double gd = 0.0, dd = 0.0;
+      for (int a = lane; a < s; a += 32) {
+        const double v = fmin(fmax(bt[a] - alpha * g[a], -M), M);
+        bn[a] = v;
+        const double d = v - bt[a];
+        gd = fma(g[a], d, gd);
+        dd = fma(d, d, dd);
+      }
+      __syncwarp();
+      double qn = 0.0, nQn = 0.0;
+      for (int a = lane; a < s; a += 32) {
+        double r = 0.0;
+        for (int b = 0; b < s; b++) r = fma(Q[a * s + b], bn[b], r);
+        qn = fma(q[a], bn[a], qn);
+        nQn = fma(bn[a], r, nQn);
+      }
+      gd = warp_sum(gd);
+      dd = warp_sum(dd);
+      qn = warp_sum(qn);
+      nQn = warp_sum(nQn);
+      f_n = 0.5 * nQn - qn;
+      const double rhs = f_t + gd + dd / (2.0 * alpha);
+      if (f_n <= rhs + 1e-15 * fabs(rhs)) break;   // eq:fpg_armijo (rounding slack)
+      alpha *= 0.5;
+    }
+    double dmax = 0.0, bmax = 0.0;
+    for (int a = lane; a < s; a += 32) {
+      dmax = fmax(dmax, fabs(bn[a] - bb[a]));
+      bmax = fmax(bmax, fabs(bn[a]));
+      bp[a] = bb[a];
+      bb[a] = bn[a];
+    }
+    __syncwarp();
+    dmax = warp_max(dmax);
+    bmax = warp_max(bmax);
+    f_cur = f_n;
+    if (dmax <= 1e-14 * (1.0 + bmax)) break;   // change in β_S below tolerance
+  }
+  if (lane == 0) obj[nd] = 0.5 * yy + f_cur + lam0 * (double)s;
+  if (beta_s)
+    for (int a = lane; a < s; a += 32) beta_s[o0 + a] = bb[a];
+}
+
+}  // namespace
+
+int upper_batch(Ctx* c, int B, const int64_t* supp_off, const int32_t* supp_idx, double* obj, double* beta_s,
+                cudaStream_t st) {
+  if (B <= 0) return L0L2_OK;
+  std::vector<int64_t> off(B + 1);
+  L0L2_CUDA(c, cudaMemcpyAsync(off.data(), supp_off, sizeof(int64_t) * (B + 1), cudaMemcpyDeviceToHost, st));
+  L0L2_CUDA(c, cudaStreamSynchronize(st));
+  int smax = 0;
+  for (int k = 0; k < B; k++) {
+    const int64_t sk = off[k + 1] - off[k];
+    if (sk < 0 || sk > c->p) return set_err(c, L0L2_EINVAL, "bad support offsets");
+    smax = std::max<int>(smax, (int)sk);
+  }
+  const size_t vec_bytes = sizeof(double) * (size_t)(6 + kRC) * smax;
+  const size_t limit = 200 * 1024;
+  int smax_smem = smax;
+  size_t smem = sizeof(double) * (size_t)smax * smax + vec_bytes;
+  double* Qg = nullptr;
+  int64_t qstride = 0;
+  if (smem > limit) {   // Gram does not fit shared memory: keep it in HBM/L2
+    smax_smem = 0;
+    smem = vec_bytes;
+    qstride = (int64_t)smax * smax;
+    if (c->ub_scratch_bytes < (size_t)B * qstride * sizeof(double)) {
+      if (c->ub_scratch) cudaFree(c->ub_scratch);
+      c->ub_scratch_bytes = (size_t)B * qstride * sizeof(double);
+      if (cudaMalloc(&c->ub_scratch, c->ub_scratch_bytes) != cudaSuccess) {
+        c->ub_scratch = nullptr;
+        c->ub_scratch_bytes = 0;
+        return set_err(c, L0L2_ENOMEM, "upper-bound Gram scratch");
+      }
+    }
+    Qg = (double*)c->ub_scratch;
+    if (smem > limit) return set_err(c, L0L2_EINVAL, "support too large (%d)", smax);
+  }
+  L0L2_CUDA(c, cudaFuncSetAttribute(fpg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit));
+  fpg_kernel<<<B, 32, smem, st>>>(c->X, c->ld, c->n, c->y, c->c, c->yy, c->lam0, c->lam2, c->M, supp_off, supp_idx,
+                                  obj, beta_s, Qg, qstride, smax_smem, 50000);
+  L0L2_LAUNCHED(c);
+  return L0L2_OK;
+}
+
+}  // namespace l0l2
