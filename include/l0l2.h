@@ -124,6 +124,7 @@ typedef struct {
   int32_t rebalance_every;  /* multi-GPU: rounds between frontier rebalancing; default 8         */
   int64_t warm_bytes_cap;   /* device bytes for parent warm states; 0 → 25% of free HBM          */
   int32_t verbose;          /* 1: one progress line per round on stderr                          */
+  int32_t record;           /* 1: keep a per-node trace of this rank (l0l2_solve_trace)           */
 } l0l2_solve_opts;
 
 void l0l2_default_solve_opts(l0l2_solve_opts* o);
@@ -156,6 +157,12 @@ typedef struct {
 int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts, double* beta, double* obj, double* gap,
                l0l2_stats* stats);
 
+/* Per-node trace of the last l0l2_solve run with opts.record = 1 (this rank's nodes, in the
+ * order they were solved).  Record r occupies rec[8r .. 8r+7] =
+ *   {node id, depth, LB, primal P(β), ADMM iterations, branch j (−1 = none), flags, UB on its support}.
+ * Returns the number of records available (may exceed max_nodes; only max_nodes are written). */
+int64_t l0l2_solve_trace(const l0l2_ctx* ctx, double* rec, int64_t max_nodes);
+
 /* Multi-GPU, one process per GPU (torch.distributed provides the process group and
  * broadcasts the id bytes).  NCCL is loaded at run time (libnccl.so.2).             */
 int l0l2_nccl_unique_id(uint8_t out[128]);
@@ -167,6 +174,19 @@ int l0l2_comm_init(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id
  * rank).  Writes up to max_moves triples (src, dst, k) into plan; returns the number of moves
  * (which may exceed max_moves), or −1 on bad arguments. */
 int l0l2_rebalance_plan(int32_t nranks, const int64_t* counts, int64_t batch, int64_t* plan, int32_t max_moves);
+
+/* Per-kernel device timing, measured with CUDA events on the stream each kernel is launched on
+ * (accumulated since l0l2_create or the last reset).  admm_*: the persistent ADMM kernel;
+ * bytes_alg / flops_alg are the ALGORITHMIC traffic / work of those launches: per iteration one
+ * read of Z (8·n·p bytes) plus the node state (β, v read + write, fixation code: 33·p bytes per
+ * node) and 4·n·p flops per node.  upper_*: the FPG kernel. */
+typedef struct {
+  int64_t admm_launches, admm_iters, admm_node_iters;
+  double  admm_ms, admm_bytes_alg, admm_flops_alg;
+  int64_t upper_launches;
+  double  upper_ms;
+} l0l2_kstats;
+int l0l2_kernel_stats(l0l2_ctx* ctx, l0l2_kstats* out, int32_t reset);
 
 /* Introspection: n, p, ρ actually used, device bytes held, and kernel launches so far. */
 int l0l2_info(const l0l2_ctx* ctx, int64_t* n, int64_t* p, double* rho, int64_t* device_bytes,

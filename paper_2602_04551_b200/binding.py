@@ -29,7 +29,7 @@ class _Opts(C.Structure):
 class _SolveOpts(C.Structure):
     _fields_ = [("gap_tol", C.c_double), ("time_limit_s", C.c_double), ("node_limit", C.c_int64),
                 ("batch", C.c_int32), ("rebalance_every", C.c_int32), ("warm_bytes_cap", C.c_int64),
-                ("verbose", C.c_int32)]
+                ("verbose", C.c_int32), ("record", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -38,6 +38,12 @@ class _Stats(C.Structure):
                 ("t_total", C.c_double), ("t_bound", C.c_double), ("t_upper", C.c_double), ("t_tree", C.c_double),
                 ("t_comm", C.c_double), ("lb", C.c_double), ("ub", C.c_double), ("gap", C.c_double),
                 ("status", C.c_int32), ("support_size", C.c_int32)]
+
+
+class _KStats(C.Structure):
+    _fields_ = [("admm_launches", C.c_int64), ("admm_iters", C.c_int64), ("admm_node_iters", C.c_int64),
+                ("admm_ms", C.c_double), ("admm_bytes_alg", C.c_double), ("admm_flops_alg", C.c_double),
+                ("upper_launches", C.c_int64), ("upper_ms", C.c_double)]
 
 
 _lib = None
@@ -76,6 +82,10 @@ def load_library():
     lib.l0l2_comm_init.restype = C.c_int
     lib.l0l2_rebalance_plan.argtypes = [C.c_int32, P, C.c_int64, P, C.c_int32]
     lib.l0l2_rebalance_plan.restype = C.c_int
+    lib.l0l2_kernel_stats.argtypes = [P, C.POINTER(_KStats), C.c_int32]
+    lib.l0l2_kernel_stats.restype = C.c_int
+    lib.l0l2_solve_trace.argtypes = [P, P, C.c_int64]
+    lib.l0l2_solve_trace.restype = C.c_int64
     lib.l0l2_info.argtypes = [P] + [P] * 5
     lib.l0l2_info.restype = C.c_int
     lib.l0l2_last_error.argtypes = [P]
@@ -187,6 +197,11 @@ class Problem:
                self._ctx)
         return dict(n=n.value, p=p.value, rho=rho.value, device_bytes=dev.value, kernel_launches=launches.value)
 
+    def l0l2_kernel_stats(self, reset=False):
+        ks = _KStats()
+        _check(self._lib.l0l2_kernel_stats(self._ctx, C.byref(ks), int(bool(reset))), self._ctx)
+        return {f: getattr(ks, f) for f, _ in _KStats._fields_}
+
     @property
     def rho(self):
         return self.info()["rho"]
@@ -269,16 +284,24 @@ class Problem:
         self.l0l2_comm_init(dist.get_world_size(), dist.get_rank(), obj[0])
 
     def l0l2_solve(self, gap_tol=1e-2, batch=16, time_limit_s=0.0, node_limit=0, rebalance_every=8,
-                   warm_bytes_cap=0, verbose=False):
+                   warm_bytes_cap=0, verbose=False, record=False):
         so = _SolveOpts()
         self._lib.l0l2_default_solve_opts(C.byref(so))
         so.gap_tol, so.batch, so.time_limit_s = float(gap_tol), int(batch), float(time_limit_s)
         so.node_limit, so.rebalance_every, so.warm_bytes_cap = int(node_limit), int(rebalance_every), int(warm_bytes_cap)
         so.verbose = int(bool(verbose))
+        so.record = int(bool(record))
         beta = np.zeros(self.p, dtype=np.float64)
         obj, gap = C.c_double(), C.c_double()
         st = _Stats()
         rc = self._lib.l0l2_solve(self._ctx, C.byref(so), beta.ctypes.data, C.byref(obj), C.byref(gap), C.byref(st))
         _check(rc, self._ctx)
         stats = {f: getattr(st, f) for f, _ in _Stats._fields_}
-        return dict(beta=beta, obj=obj.value, gap=gap.value, support=np.nonzero(beta)[0], stats=stats, rc=rc)
+        out = dict(beta=beta, obj=obj.value, gap=gap.value, support=np.nonzero(beta)[0], stats=stats, rc=rc)
+        if record:
+            nrec = self._lib.l0l2_solve_trace(self._ctx, None, 0)
+            buf = np.zeros((max(1, nrec), 8))
+            self._lib.l0l2_solve_trace(self._ctx, buf.ctypes.data, nrec)
+            out["trace"] = [dict(id=int(r[0]), depth=int(r[1]), lb=r[2], primal=r[3], iters=int(r[4]),
+                                 branch_j=int(r[5]), flags=int(r[6]), ub=r[7]) for r in buf[:nrec]]
+        return out

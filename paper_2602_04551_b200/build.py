@@ -30,7 +30,8 @@ def build(verbose=False, force=False):
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     inc = _nccl_include()
-    flags = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+    extra = os.environ.get("L0L2_NVCC_FLAGS", "").split()
+    flags = extra + ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
                     "-I", inc, "-I", os.path.join(HERE, "..", "include")]
     objs = []
     newest_src = max(os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC))

@@ -23,6 +23,7 @@
 //   primal P(β) = ½‖y‖² − cᵀβ + ½‖L(Zβ)‖² + Σ ψ_j(β_j)
 // where Zβ is one extra forward-only sweep on check iterations.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -30,7 +31,6 @@ namespace l0l2 {
 namespace {
 
 constexpr int NW = kAdmmThreads / 32;   // 16 warps
-constexpr int MAXMT = 9;                // ≤ 9 row tiles of 8 per warp → n ≤ 16·9·8 = 1152
 constexpr int F_ACTIVE = 8;             // internal node flag bit (not exported)
 
 struct KP {
@@ -64,18 +64,36 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
 }
+#ifndef L0L2_DEBUG_HANG
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned phase) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(saddr(b)), "r"(phase) : "memory");
 }
+#else
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned phase) {
+  for (long long spin = 0;; spin++) {
+    unsigned ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok) : "r"(saddr(b)), "r"(phase) : "memory");
+    if (ok) return;
+    if (spin == 2000000) {
+      printf("HANG mbar blk %d tid %d bar %p phase %u\n", blockIdx.x, threadIdx.x, b, phase);
+      __trap();
+    }
+  }
+}
+#endif
 // TMA bulk copy global → shared (SASS UBLKCP), completion counted on the mbarrier
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(saddr(dst)),
       "l"(src), "r"(bytes), "r"(saddr(b))
       : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
@@ -137,95 +155,164 @@ __device__ __forceinline__ double nu_f(const KP& k, double x, uint8_t code) {   
 }
 
 // ---------------------------------------------------------------- shared memory layout
+constexpr int NST = 3;         // Z tile stages in the TMA ring
+constexpr int PFD = 3;         // additional tiles prefetched into L2 beyond the smem ring
+constexpr int NMW = NW - 2;    // MMA warps (adjoint + forward); the last 2 warps run the epilogue
+constexpr int MMA_THREADS = NMW * 32;
+constexpr int MAXKS = 26;      // adjoint k-steps (4 rows each) per MMA warp held in registers
+constexpr int MAXMT2 = 13;     // forward row tiles (8 rows) per MMA warp  → n ≤ 10·13·8 = 1040
+// named barriers (id 0 is __syncthreads)
+constexpr int BAR_ADJ = 1;     // +0/+1 (double buffered): MMA → epilogue "S_J partials ready"
+constexpr int BAR_EPI = 3;     // +0/+1: epilogue → MMA "w⁺_J ready"
+constexpr int BAR_MMA = 5;     // MMA warps only: "tile stage released"
+
 struct Smem {
-  double* Us;      // [kBC][ld]   u of this iteration (node-major)
-  double* tile[2]; // [kPt][ld]   two Z_J buffers
-  double* spart;   // [NW][64]    adjoint partials per warp
-  double* Ws;      // [kBC][12]   w⁺_J (node-major, padded)
-  double* red;     // [kBC][kSums] scratch
-  uint64_t* mbar;  // [3]: tile0, tile1, U
-  int* flags;      // [kBC]
+  double* tiles;      // [NST][kPt][ld]   Z_J ring (stage q at tiles + q·kPt·ld)
+  double* spart;      // [2][NMW][64]     adjoint partials per MMA warp (double buffered)
+  double* Ws;         // [2][kBC][12]     w⁺_J (node-major, padded; double buffered)
+  double* red;        // [kBC]            running max of checked duals (R7)
+  uint64_t* mbar;     // [NST]
+  int* flags;         // [kBC]
 };
+
+// Named barriers.  The warp is re-converged first: lane 0 of MMA warp 0 diverges to issue TMA
+// refills, and the .aligned forms (bar.sync / bar.arrive) require a converged warp.
+__device__ __forceinline__ void nbar_sync(int id, int cnt) {
+  __syncwarp();
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int cnt) {
+  __syncwarp();
+  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
 
 enum { SW_FWD_W = 0, SW_FWD_BETA = 1, SW_FUSED = 2 };
 
-// One sweep over this CTA's tiles.  Forward partials go to Upart[cta]; check sums to sums[cta].
-__device__ void sweep(const KP& k, Smem& s, int mode, bool refresh, bool check, unsigned& phase0,
-                      unsigned& phase1, unsigned& phaseU) {
+// One sweep over this CTA's tiles, warp-specialised:
+//   MMA warps (0..NMW−1):  adj(t0); for t: [adj(t+1)] → wait w⁺(t) → fwd(t) → release stage(t)
+//   epilogue warps:        for t: wait S(t) → b, β⁺, v⁺, w⁺, check sums → publish w⁺(t)
+// so the elementwise epilogue of tile t overlaps the DMMA adjoint of tile t+1.  u of this
+// iteration lives in registers as the adjoint's B fragments (MMA warp w owns k-steps [ks0, ks1),
+// lane holds U[row = 4q + lane%4][node = lane/4]).  Forward partials go to Upart[cta], check sums
+// to sums[cta].
+template <int MODE>
+__device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& phases) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.x, G = gridDim.x;
   const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
-  const int mt = (int)(k.n8 / 8);            // row tiles of the forward product
-  const int kt = (int)(k.n8 / 4);            // k-steps of the adjoint
-  const int ks0 = kt * warp / NW, ks1 = kt * (warp + 1) / NW;
   const unsigned tile_bytes = (unsigned)(kPt * k.ld * sizeof(double));
-  const bool fused = (mode == SW_FUSED);
+  constexpr bool fused = (MODE == SW_FUSED);
+  const bool is_mma = warp < NMW;
 
-  double acc[MAXMT][2];
+  if (is_mma) {
+    const int mt = (int)(k.n8 / 8);
+    const int kt = (int)(k.n8 / 4);
+    const int ks0 = kt * warp / NMW, ks1 = kt * (warp + 1) / NMW;
+    double acc[MAXMT2][2];
 #pragma unroll
-  for (int i = 0; i < MAXMT; i++) acc[i][0] = acc[i][1] = 0.0;
-  // per-thread check sums for (j = tid>>3, node = tid&7), tid < 64
-  double sT1 = 0.0, sT2 = 0.0, sT3 = 0.0, sT4 = 0.0;
-
-  if (fused) {   // u of this iteration → shared memory (written by the previous reduce phase)
-    if (tid == 0) {
-      fence_proxy_async_global();
-      fence_proxy_async_smem();
-      mbar_expect_tx(&s.mbar[2], (unsigned)(kBC * k.ld * sizeof(double)));
-      bulk_g2s(s.Us, k.U, (unsigned)(kBC * k.ld * sizeof(double)), &s.mbar[2]);
-    }
-  }
-  if (tid == 0 && t0 < t1) {
-    fence_proxy_async_smem();
-    mbar_expect_tx(&s.mbar[0], tile_bytes);
-    bulk_g2s(s.tile[0], k.Z + (int64_t)t0 * kPt * k.ld, tile_bytes, &s.mbar[0]);
-  }
-  if (fused) { mbar_wait(&s.mbar[2], phaseU); phaseU ^= 1u; }
-
-  for (int t = t0; t < t1; t++) {
-    const int buf = (t - t0) & 1;
-    // prefetch the next tile into the other buffer (freed by the __syncthreads at the end of t−1)
-    if (tid == 0 && t + 1 < t1) {
-      fence_proxy_async_smem();
-      mbar_expect_tx(&s.mbar[buf ^ 1], tile_bytes);
-      bulk_g2s(s.tile[buf ^ 1], k.Z + (int64_t)(t + 1) * kPt * k.ld, tile_bytes, &s.mbar[buf ^ 1]);
-    }
-    const int64_t col0 = (int64_t)t * kPt;
-    // Issue the state loads for the epilogue before waiting on the tile.
-    double st_beta = 0.0, st_v = 0.0, st_c = 0.0;
-    uint8_t st_code = 1;
-    if (tid < 64) {
-      const int j = tid >> 3, nd = tid & 7;
-      const int64_t e = (col0 + j) * kBC + nd;
-      st_beta = k.beta[e];
-      st_v = k.v[e];
-      st_c = k.c[col0 + j];
-      st_code = k.code[e];
-    }
-    if (buf == 0) { mbar_wait(&s.mbar[0], phase0); phase0 ^= 1u; }
-    else { mbar_wait(&s.mbar[1], phase1); phase1 ^= 1u; }
-    const double* T = s.tile[buf];
-
+    for (int i = 0; i < MAXMT2; i++) acc[i][0] = acc[i][1] = 0.0;
+    double uf[MAXKS];
     if (fused) {
-      // ---- adjoint: S_J(8 cols × 8 nodes) = Z_Jᵀ U, K = rows split across warps
-      double sc[2] = {0.0, 0.0};
-      for (int q = ks0; q < ks1; q++) {
-        const int r = q * 4 + (lane & 3);
-        double a = T[(lane >> 2) * k.ld + r];          // A[m = col][k = row]
-        double b = s.Us[(lane >> 2) * k.ld + r];       // B[k = row][n = node]
-        dmma(sc, a, b);
+#pragma unroll
+      for (int qi = 0; qi < MAXKS; qi++) {
+        const int q = ks0 + qi;
+        uf[qi] = (q < ks1) ? __ldcg(k.U + (lane >> 2) * k.ld + q * 4 + (lane & 3)) : 0.0;
       }
+    }
+    // prologue: fill NST stages, prefetch PFD more tiles into L2
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      for (int t = t0; t < t1 && t < t0 + NST; t++) {
+        const int sg = (t - t0) % NST;
+        mbar_expect_tx(&s.mbar[sg], tile_bytes);
+        bulk_g2s(s.tiles + (size_t)sg * kPt * k.ld, k.Z + (int64_t)t * kPt * k.ld, tile_bytes, &s.mbar[sg]);
+      }
+      for (int t = t0 + NST; t < t1 && t < t0 + NST + PFD; t++) prefetch_l2(k.Z + (int64_t)t * kPt * k.ld, tile_bytes);
+    }
+    auto adjoint = [&](int t) {
+      const int sg = (t - t0) % NST;
+      mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
+      phases ^= 1u << sg;
+      const double* T = s.tiles + (size_t)sg * kPt * k.ld;
+      double sc0[2] = {0.0, 0.0}, sc1[2] = {0.0, 0.0};
+#pragma unroll
+      for (int qi = 0; qi < MAXKS; qi += 2) {
+        if (ks0 + qi < ks1) dmma(sc0, T[(lane >> 2) * k.ld + (ks0 + qi) * 4 + (lane & 3)], uf[qi]);
+        if (ks0 + qi + 1 < ks1) dmma(sc1, T[(lane >> 2) * k.ld + (ks0 + qi + 1) * 4 + (lane & 3)], uf[qi + 1]);
+      }
+      double* sp = s.spart + ((t - t0) & 1) * NMW * 64 + warp * 64;
       // C fragment: row (col j) = lane>>2, cols (node) = 2*(lane&3) + {0,1}
-      s.spart[warp * 64 + (lane >> 2) * 8 + 2 * (lane & 3)] = sc[0];
-      s.spart[warp * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = sc[1];
-      __syncthreads();
-      if (tid < 64) {
-        const int j = tid >> 3, nd = tid & 7;
+      sp[(lane >> 2) * 8 + 2 * (lane & 3)] = sc0[0] + sc1[0];
+      sp[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = sc0[1] + sc1[1];
+      nbar_arrive(BAR_ADJ + ((t - t0) & 1), kAdmmThreads);
+    };
+    if (fused && t0 < t1) adjoint(t0);
+    if (!fused) {   // grant the two w⁺ buffers to the epilogue warps (no adjoint to pace them)
+      if (t0 < t1) nbar_arrive(BAR_ADJ + 0, kAdmmThreads);
+      if (t0 + 1 < t1) nbar_arrive(BAR_ADJ + 1, kAdmmThreads);
+    }
+    for (int t = t0; t < t1; t++) {
+      if (fused && t + 1 < t1) adjoint(t + 1);
+      const int sg = (t - t0) % NST;
+      if (!fused) {
+        mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
+        phases ^= 1u << sg;
+      }
+      nbar_sync(BAR_EPI + ((t - t0) & 1), kAdmmThreads);   // w⁺_J(t) published
+      const double* T = s.tiles + (size_t)sg * kPt * k.ld;
+      const double* W = s.Ws + ((t - t0) & 1) * kBC * 12;
+      // ---- forward: U⁺(rows × 8 nodes) += Z_J (rows × 8 cols) · W_J (8 cols × 8 nodes)
+      const double b0 = W[(lane >> 2) * 12 + (lane & 3)];         // B[k = j][n = node]
+      const double b1 = W[(lane >> 2) * 12 + 4 + (lane & 3)];
+#pragma unroll
+      for (int i = 0; i < MAXMT2; i++) {
+        const int m = warp + i * NMW;
+        if (m < mt) {
+          const int row = m * 8 + (lane >> 2);
+          dmma(acc[i], T[(lane & 3) * k.ld + row], b0);            // A[m = row][k = col j]
+          dmma(acc[i], T[(4 + (lane & 3)) * k.ld + row], b1);
+        }
+      }
+      if (!fused && t + 2 < t1) nbar_arrive(BAR_ADJ + ((t - t0) & 1), kAdmmThreads);   // w⁺ buffer free for t+2
+      nbar_sync(BAR_MMA, MMA_THREADS);                             // every MMA warp is done with stage(t)
+      if (tid == 0 && t + NST < t1) {
+        fence_proxy_async_smem();
+        mbar_expect_tx(&s.mbar[sg], tile_bytes);
+        bulk_g2s(s.tiles + (size_t)sg * kPt * k.ld, k.Z + (int64_t)(t + NST) * kPt * k.ld, tile_bytes, &s.mbar[sg]);
+        if (t + NST + PFD < t1) prefetch_l2(k.Z + (int64_t)(t + NST + PFD) * kPt * k.ld, tile_bytes);
+      }
+      __syncwarp();
+    }
+    // ---- this CTA's forward partial: Upart[g][node][row]
+    double* up = k.Upart + (int64_t)g * kBC * k.ld;
+#pragma unroll
+    for (int i = 0; i < MAXMT2; i++) {
+      const int m = warp + i * NMW;
+      if (m < mt) {
+        const int row = m * 8 + (lane >> 2), nd = 2 * (lane & 3);
+        up[(int64_t)nd * k.ld + row] = acc[i][0];
+        up[(int64_t)(nd + 1) * k.ld + row] = acc[i][1];
+      }
+    }
+  } else {
+    // ---------------- epilogue warps: element (j = et>>3, node = et&7) of each 8×8 block
+    const int et = tid - MMA_THREADS, j = et >> 3, nd = et & 7;
+    const bool active = (s.flags[nd] & F_ACTIVE) != 0;
+    double sT1 = 0.0, sT2 = 0.0, sT3 = 0.0, sT4 = 0.0;
+    for (int t = t0; t < t1; t++) {
+      const int64_t col0 = (int64_t)t * kPt;
+      const int64_t e = (col0 + j) * kBC + nd;
+      const double st_beta = k.beta[e], st_v = k.v[e], st_c = k.c[col0 + j];
+      const uint8_t st_code = k.code[e];
+      double wn = 0.0;
+      // fused: S_J(t) partials written; forward-only: w⁺ buffer (t−t0)&1 released by the MMA warps
+      nbar_sync(BAR_ADJ + ((t - t0) & 1), kAdmmThreads);
+      if (fused) {
+        const double* sp = s.spart + ((t - t0) & 1) * NMW * 64;
         double sv = 0.0;
 #pragma unroll
-        for (int w = 0; w < NW; w++) sv += s.spart[w * 64 + j * 8 + nd];   // fixed order
-        double wn = 0.0;
-        if (s.flags[nd] & F_ACTIVE) {
+        for (int w = 0; w < NMW; w++) sv += sp[w * 64 + j * 8 + nd];   // fixed order
+        if (active) {
           const double w = st_c + k.rho * st_beta - st_v;
           const double b = (w - sv) * k.inv_rho;
           const double bn = refresh ? st_beta : prox(k, b + st_v * k.inv_rho, st_code);
@@ -235,68 +322,32 @@ __device__ void sweep(const KP& k, Smem& s, int mode, bool refresh, bool check, 
             sT2 += nu_f(k, fabs(st_c - sv), st_code);
             sT3 = fma(st_c, bn, sT3);
             sT4 += psi_f(k, bn, st_code);
-            k.bchk[(col0 + j) * kBC + nd] = b;
+            k.bchk[e] = b;
           }
-          const int64_t e = (col0 + j) * kBC + nd;
           k.beta[e] = bn;
           k.v[e] = vn;
           wn = st_c + k.rho * bn - vn;
         }
-        s.Ws[nd * 12 + j] = wn;
+      } else if (active) {
+        wn = (MODE == SW_FWD_BETA) ? st_beta : st_c + k.rho * st_beta - st_v;
       }
-      __syncthreads();
-    } else {
-      if (tid < 64) {
-        const int j = tid >> 3, nd = tid & 7;
-        double wn = 0.0;
-        if (s.flags[nd] & F_ACTIVE)
-          wn = (mode == SW_FWD_BETA) ? st_beta : st_c + k.rho * st_beta - st_v;
-        s.Ws[nd * 12 + j] = wn;
-      }
-      __syncthreads();
+      s.Ws[((t - t0) & 1) * kBC * 12 + nd * 12 + j] = wn;
+      nbar_arrive(BAR_EPI + ((t - t0) & 1), kAdmmThreads);
     }
-    // ---- forward: U⁺(rows × 8 nodes) += Z_J (rows × 8 cols) · W_J (8 cols × 8 nodes)
-    {
-      const double b0 = s.Ws[(lane >> 2) * 12 + (lane & 3)];       // B[k = j][n = node]
-      const double b1 = s.Ws[(lane >> 2) * 12 + 4 + (lane & 3)];
-#pragma unroll
-      for (int i = 0; i < MAXMT; i++) {
-        const int m = warp + i * NW;
-        if (m < mt) {
-          const int row = m * 8 + (lane >> 2);
-          double a0 = T[(lane & 3) * k.ld + row];                  // A[m = row][k = col j]
-          double a1 = T[(4 + (lane & 3)) * k.ld + row];
-          dmma(acc[i], a0, b0);
-          dmma(acc[i], a1, b1);
-        }
-      }
-    }
-    __syncthreads();   // tile buffer and Ws free for reuse
-  }
-  // ---- write this CTA's forward partial: Upart[g][node][row]
-  double* up = k.Upart + (int64_t)g * kBC * k.ld;
-#pragma unroll
-  for (int i = 0; i < MAXMT; i++) {
-    const int m = warp + i * NW;
-    if (m < mt) {
-      const int row = m * 8 + (lane >> 2), nd = 2 * (lane & 3);
-      up[(int64_t)nd * k.ld + row] = (t0 < t1) ? acc[i][0] : 0.0;
-      up[(int64_t)(nd + 1) * k.ld + row] = (t0 < t1) ? acc[i][1] : 0.0;
+    if (fused && check) {
+      // stash per-thread sums; reduced below after the CTA barrier
+      s.Ws[2 * kBC * 12 + et * 4 + 0] = sT1;
+      s.Ws[2 * kBC * 12 + et * 4 + 1] = sT2;
+      s.Ws[2 * kBC * 12 + et * 4 + 2] = sT3;
+      s.Ws[2 * kBC * 12 + et * 4 + 3] = sT4;
     }
   }
-  if (check && fused) {
-    // reduce the 8 column-threads of each node in a fixed order
-    if (tid < 64) {
-      s.spart[tid * 4 + 0] = sT1; s.spart[tid * 4 + 1] = sT2;
-      s.spart[tid * 4 + 2] = sT3; s.spart[tid * 4 + 3] = sT4;
-    }
-    __syncthreads();
-    if (tid < kBC * 4) {
-      const int nd = tid >> 2, q = tid & 3;
-      double a = 0.0;
-      for (int j = 0; j < 8; j++) a += s.spart[(j * 8 + nd) * 4 + q];
-      k.sums[((int64_t)g * kBC + nd) * kSums + q] = a;
-    }
+  __syncthreads();
+  if (fused && check && tid < kBC * 4) {
+    const int nd = tid >> 2, q = tid & 3;
+    double a = 0.0;
+    for (int j = 0; j < 8; j++) a += s.Ws[2 * kBC * 12 + (j * 8 + nd) * 4 + q];
+    k.sums[((int64_t)g * kBC + nd) * kSums + q] = a;
   }
 }
 
@@ -357,20 +408,16 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   Smem s;
   {
     double* base = reinterpret_cast<double*>(smem_raw);
-    s.Us = base;
-    s.tile[0] = s.Us + kBC * k.ld;
-    s.tile[1] = s.tile[0] + kPt * k.ld;
-    s.spart = s.tile[1] + kPt * k.ld;
-    s.Ws = s.spart + NW * 64;
-    s.red = s.Ws + kBC * 12;
-    s.mbar = reinterpret_cast<uint64_t*>(s.red + kBC * kSums);
-    s.flags = reinterpret_cast<int*>(s.mbar + 4);
+    s.tiles = base;
+    s.spart = base + (size_t)NST * kPt * k.ld;
+    s.Ws = s.spart + 2 * NMW * 64;
+    s.red = s.Ws + 2 * kBC * 12 + 64 * 4;
+    s.mbar = reinterpret_cast<uint64_t*>(s.red + kBC);
+    s.flags = reinterpret_cast<int*>(s.mbar + NST);
   }
   const int tid = threadIdx.x;
   if (tid == 0) {
-    mbar_init(&s.mbar[0], 1);
-    mbar_init(&s.mbar[1], 1);
-    mbar_init(&s.mbar[2], 1);
+    for (int q = 0; q < NST; q++) mbar_init(&s.mbar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < kBC) {
@@ -378,26 +425,26 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     s.red[tid] = -INFINITY;
   }
   __syncthreads();
-  unsigned ph0 = 0, ph1 = 0, phU = 0;
+  unsigned phases = 0;
 
   // u0 = Z (c + ρβ0 − v0), then the warm/cold refresh sweep (R6)
-  sweep(k, s, SW_FWD_W, false, false, ph0, ph1, phU);
+  sweep<SW_FWD_W>(k, s, false, false, phases);
   grid_sync(k.bar);
   reduce_u(k, k.U);
   grid_sync(k.bar);
-  sweep(k, s, SW_FUSED, true, false, ph0, ph1, phU);
+  sweep<SW_FUSED>(k, s, true, false, phases);
   grid_sync(k.bar);
   reduce_u(k, k.U);
   grid_sync(k.bar);
 
   for (int it = 1; it <= k.max_iters; it++) {
     const bool chk = (it % k.check_every == 0) || (it == k.max_iters);
-    sweep(k, s, SW_FUSED, false, chk, ph0, ph1, phU);
+    sweep<SW_FUSED>(k, s, false, chk, phases);
     grid_sync(k.bar);
     reduce_u(k, k.U);
     grid_sync(k.bar);
     if (!chk) continue;
-    sweep(k, s, SW_FWD_BETA, false, false, ph0, ph1, phU);
+    sweep<SW_FWD_BETA>(k, s, false, false, phases);
     grid_sync(k.bar);
     reduce_u(k, k.Ub);
     grid_sync(k.bar);
@@ -589,15 +636,17 @@ __global__ void fill_y(double* r, int64_t ldr, const double* y, int64_t n, int n
 }  // namespace
 
 size_t admm_smem_bytes(int64_t ld) {
-  return sizeof(double) * ((size_t)kBC * ld + 2 * (size_t)kPt * ld + NW * 64 + kBC * 12 + kBC * kSums) +
-         4 * sizeof(uint64_t) + kBC * sizeof(int) + 64;
+  return sizeof(double) * ((size_t)NST * kPt * ld + 2 * NMW * 64 + 2 * kBC * 12 + 64 * 4 + kBC) +
+         NST * sizeof(uint64_t) + kBC * sizeof(int) + 64;
 }
 
 int admm_alloc(Ctx* c) {
   const int64_t p8 = round8(c->p), ld = c->ld;
-  if (round8(c->n) / 8 > NW * MAXMT) return set_err(c, L0L2_EINVAL, "n = %lld > %d not supported by the fused ADMM kernel", (long long)c->n, NW * MAXMT * 8);
+  if (round8(c->n) / 8 > NMW * MAXMT2 || round8(c->n) / 4 > NMW * MAXKS)
+    return set_err(c, L0L2_EINVAL, "n = %lld > %d not supported by the fused ADMM kernel", (long long)c->n, NMW * MAXMT2 * 8);
   const int ntiles = (int)(p8 / kPt);
   c->grid = std::min(c->sms, ntiles);
+  if (const char* e = getenv("L0L2_GRID")) c->grid = std::max(1, std::min(c->grid, atoi(e)));   // testing hook
   c->beta = (double*)dalloc(c, sizeof(double) * p8 * kBC);
   c->v = (double*)dalloc(c, sizeof(double) * p8 * kBC);
   c->bchk = (double*)dalloc(c, sizeof(double) * p8 * kBC);
@@ -667,9 +716,32 @@ int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st) {
   k.psi_l1 = 2.0 * std::sqrt(c->lam0 * c->lam2);
   k.psi_4 = c->lam0 / c->M + c->lam2 * c->M;
   void* args[] = {&k};
+  if (!c->ev[0]) {
+    for (auto& e : c->ev) L0L2_CUDA(c, cudaEventCreate(&e));
+  }
+  L0L2_CUDA(c, cudaEventRecord(c->ev[0], st));
   L0L2_CUDA(c, cudaLaunchCooperativeKernel((void*)admm_persistent, dim3(c->grid), dim3(kAdmmThreads), args,
                                            admm_smem_bytes(c->ld), st));
   L0L2_LAUNCHED(c);
+  L0L2_CUDA(c, cudaEventRecord(c->ev[1], st));
+  return L0L2_OK;
+}
+
+// Called after the stream has been synchronised past run_admm: accumulate the event-timed
+// duration and the algorithmic work of the launch (iterations = max over its nodes + refresh).
+int account_admm(Ctx* c, int nb, const int* iters_host) {
+  float ms = 0.f;
+  L0L2_CUDA(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  int64_t tmax = 0, tsum = 0;
+  for (int k = 0; k < nb; k++) { tmax = std::max<int64_t>(tmax, iters_host[k]); tsum += iters_host[k]; }
+  const double T = (double)(tmax + 1);   // + the refresh sweep
+  const double n = (double)c->n, p = (double)c->p;
+  c->ks.admm_launches++;
+  c->ks.admm_iters += tmax + 1;
+  c->ks.admm_node_iters += tsum;
+  c->ks.admm_ms += ms;
+  c->ks.admm_bytes_alg += T * (8.0 * n * p + 33.0 * p * nb);
+  c->ks.admm_flops_alg += (double)(tsum + nb) * 4.0 * n * p;
   return L0L2_OK;
 }
 

@@ -73,6 +73,7 @@ void l0l2_destroy(l0l2_ctx* ctx) {
   for (void* p : c->owned) cudaFree(p);
   if (c->ub_scratch) cudaFree(c->ub_scratch);
   for (void* s : c->scr) if (s) cudaFree(s);
+  for (auto e : c->ev) if (e) cudaEventDestroy(e);
   comm_free(c);
   delete ctx;
 }
@@ -234,11 +235,23 @@ int l0l2_bound_batch(l0l2_ctx* ctx, int32_t B, const int64_t* fix_off, const int
       if (rc) return rc;
     }
     uint8_t hf[kBC];
+    int32_t hit[kBC];
     L0L2_CUDA(c, cudaMemcpyAsync(hf, flags + g0, nb, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(hit, iters + g0, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
     L0L2_CUDA(c, cudaStreamSynchronize(st));
+    rc = account_admm(c, nb, hit);
+    if (rc) return rc;
     for (int k = 0; k < nb; k++) notconv |= (hf[k] & L0L2_FLAG_MAXITER) != 0;
   }
   return notconv ? L0L2_WNOTCONV : L0L2_OK;
+}
+
+int l0l2_kernel_stats(l0l2_ctx* ctx, l0l2_kstats* out, int32_t reset) {
+  if (!ctx) return L0L2_EINVAL;
+  Ctx* c = &ctx->impl;
+  if (out) *out = c->ks;
+  if (reset) c->ks = l0l2_kstats{};
+  return L0L2_OK;
 }
 
 int l0l2_upper_batch(l0l2_ctx* ctx, int32_t B, const int64_t* supp_off, const int32_t* supp_idx, double* obj,

@@ -12,7 +12,7 @@ namespace l0l2 {
 
 constexpr int kBC = 8;          // node columns per ADMM pass (DMMA n-dim = 8)
 constexpr int kPt = 8;          // Z columns per tile (DMMA m-dim of the adjoint = 8)
-constexpr int kAdmmThreads = 512;  // 16 warps per persistent CTA
+constexpr int kAdmmThreads = 384;  // 12 warps per persistent CTA
 constexpr int kSums = 6;        // per-node partial sums of a check (see admm.cu)
 
 // leading dimension of Z / X in HBM: ≥ n, even, ≡ 4 (mod 16) doubles so that the 8-byte
@@ -73,6 +73,10 @@ struct Ctx {
   }
   void* scratch(size_t b) { return scratch_n(0, b); }
   void* scratch2(size_t b) { return scratch_n(1, b); }
+  std::vector<double> trace;   // l0l2_solve_trace records (8 doubles per node)
+  // live kernel timing (l0l2_kernel_stats)
+  l0l2_kstats ks{};
+  cudaEvent_t ev[4] = {};
   // multi-GPU
   int nranks = 1, rank = 0;
   void* nccl_comm = nullptr;
@@ -120,6 +124,7 @@ struct BoundArgs {
 int pack_group(Ctx* c, int nb, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
                const double* const* warm_ptrs_dev, cudaStream_t st);
 int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st);
+int account_admm(Ctx* c, int nb, const int* iters_host);
 int finalize_group(Ctx* c, int nb, double* zhat, int32_t* branch_j, uint8_t* flags,
                    int32_t* supp_cnt, int32_t* supp_idx, int64_t supp_stride, cudaStream_t st);
 int unpack_warm(Ctx* c, int nb, double* const* warm_ptrs_dev, cudaStream_t st);

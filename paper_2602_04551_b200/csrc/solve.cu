@@ -195,6 +195,7 @@ struct Solver {
   int64_t next_id = 1, nodes = 0, node_iters = 0, rounds = 0, max_open = 0;
   double t_bound = 0, t_upper = 0, t_tree = 0, t_comm = 0;
   bool notconv = false;
+  std::vector<double>* trace = nullptr;
   // multi-rank
   int W = 1, R = 0;
   bool partitioned = false;
@@ -283,7 +284,10 @@ struct Solver {
       if ((rc = unpack_warm(c, nb, d.wptr + kBC, st))) return rc;
       // supports of this group → host (counts first)
       L0L2_CUDA(c, cudaMemcpyAsync(scnt.data() + g0, d.scnt + g0, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+      int32_t hit_g[kBC];
+      L0L2_CUDA(c, cudaMemcpyAsync(hit_g, d.iters + g0, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
       L0L2_CUDA(c, cudaStreamSynchronize(st));
+      if ((rc = account_admm(c, nb, hit_g))) return rc;
       for (int k = 0; k < nb; k++) {
         res[g0 + k].supp.resize(scnt[g0 + k]);
         if (scnt[g0 + k] > 0)
@@ -353,6 +357,13 @@ struct Solver {
         inc_S = res[k].supp;
         inc_b = res[k].beta_s;
         ub_owner = R;
+      }
+    if (trace)
+      for (int k : order) {
+        const Res& r = res[k];
+        const double rec[8] = {(double)batch[k].id, (double)batch[k].depth, r.lb, r.primal, (double)r.iters,
+                               (double)r.branch, (double)r.flags, r.obj};
+        trace->insert(trace->end(), rec, rec + 8);
       }
     for (int k : order) {
       Res& r = res[k];
@@ -534,6 +545,7 @@ void l0l2_default_solve_opts(l0l2_solve_opts* o) {
   o->rebalance_every = 8;
   o->warm_bytes_cap = 0;
   o->verbose = 0;
+  o->record = 0;
 }
 
 int l0l2_nccl_unique_id(uint8_t out[128]) {
@@ -567,6 +579,14 @@ int l0l2_comm_init(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id
   c->nranks = nranks;
   c->rank = rank;
   return L0L2_OK;
+}
+
+int64_t l0l2_solve_trace(const l0l2_ctx* ctx, double* rec, int64_t max_nodes) {
+  if (!ctx) return -1;
+  const std::vector<double>& t = ctx->impl.trace;
+  const int64_t n = (int64_t)t.size() / 8;
+  if (rec && max_nodes > 0) std::memcpy(rec, t.data(), sizeof(double) * 8 * std::min(n, max_nodes));
+  return n;
 }
 
 int l0l2_rebalance_plan(int32_t nranks, const int64_t* counts, int64_t batch, int64_t* plan, int32_t max_moves) {
@@ -604,6 +624,8 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
     size_t capb = o.warm_bytes_cap > 0 ? (size_t)o.warm_bytes_cap : fr / 4;
     S.pool.cap = std::max<size_t>(SlotPool::kPerChunk, capb / (sizeof(double) * 2 * c->p));
   }
+  c->trace.clear();
+  if (o.record) S.trace = &c->trace;
   int rc = S.alloc_bufs(o.batch);
   if (rc) return rc;
   S.UB = 0.5 * c->yy;   // β = 0 is feasible

@@ -191,9 +191,19 @@ int upper_batch(Ctx* c, int B, const int64_t* supp_off, const int32_t* supp_idx,
     if (smem > limit) return set_err(c, L0L2_EINVAL, "support too large (%d)", smax);
   }
   L0L2_CUDA(c, cudaFuncSetAttribute(fpg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit));
+  if (!c->ev[2]) {
+    for (auto& e : c->ev) if (!e) L0L2_CUDA(c, cudaEventCreate(&e));
+  }
+  L0L2_CUDA(c, cudaEventRecord(c->ev[2], st));
   fpg_kernel<<<B, 32, smem, st>>>(c->X, c->ld, c->n, c->y, c->c, c->yy, c->lam0, c->lam2, c->M, supp_off, supp_idx,
                                   obj, beta_s, Qg, qstride, smax_smem, 50000);
   L0L2_LAUNCHED(c);
+  L0L2_CUDA(c, cudaEventRecord(c->ev[3], st));
+  L0L2_CUDA(c, cudaEventSynchronize(c->ev[3]));
+  float ms = 0.f;
+  L0L2_CUDA(c, cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
+  c->ks.upper_launches++;
+  c->ks.upper_ms += ms;
   return L0L2_OK;
 }
 
