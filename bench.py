@@ -2,9 +2,12 @@
 """Benchmark of the B200 ℓ0–ℓ2 BnB hot path (BASELINE.json metric: BnB nodes/sec and
 time-to-certified-optimality; roofline of the ADMM kernel).
 
-One "step" = one l0l2_solve of the C4 instance (n=1000, p=1e5, k*=10, corr 0.1, SNR 5, seed 0)
-to the certified gap: every §8(a) row (pack, batched ADMM bound, check, finalize, FPG upper
-bound, frontier update, multi-GPU exchange) runs inside it.  X and y are HBM-resident (create
+One "step" = one l0l2_solve of the C4 instance (n=1000, p=1e5, k*=10, corr 0.1, SNR 5, seed 0,
+λ2*, λ0*, M from the input recipe) for a fixed, deterministic prefix of the best-first tree
+(--node-limit nodes, gap_tol 1e-2, node_tol 1e-4 as in the paper): every §8(a) row (pack,
+batched ADMM bound, check, finalize, FPG upper bound, frontier update, multi-GPU exchange) runs
+inside it.  (With the recipe's λ2* = 1e-4 the C4 relaxation is weak and the tree does not close
+in minutes, so the step is a tree prefix; the certified gap it reaches is reported.)  X and y are HBM-resident (create
 done before the timed region) for `value`; `e2e` re-runs the whole thing through the public
 API from pinned host buffers (create = H2D + precompute, solve, β* back to host).
 
@@ -43,10 +46,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--gap-tol", type=float, default=1e-6)
-    ap.add_argument("--node-tol", type=float, default=1e-8)
+    ap.add_argument("--gap-tol", type=float, default=1e-2)
+    ap.add_argument("--node-tol", type=float, default=1e-4)
+    ap.add_argument("--node-limit", type=int, default=512)
     ap.add_argument("--batch", type=int, default=16)
-    ap.add_argument("--rho-mult", type=float, default=1.0)
+    ap.add_argument("--rho-mult", type=float, default=3.0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -125,9 +129,22 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def oracle_iters_per_node(cfg):
+    """Mean ADMM iterations per node of the oracle's own tree prefix on this config
+    (tests/golden/oracle_<cfg>_prefix.json, written by tools/oracle_c4_prefix.py from oracle/ only)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "oracle_%s_prefix.json" % cfg)) as f:
+            d = json.load(f)
+        return float(d["iters_per_node"]), int(d["nodes"])
+    except Exception:
+        return None, 0
+
+
 def cpu_baseline(inst, args, rho, seconds):
-    """The oracle as it stands (numpy, float64) on the box's host cores: its own BnB on the same
-    instance for a bounded wall-clock budget; nodes solved / time."""
+    """The oracle as it stands (numpy fp64) on the box's host cores.  A whole oracle node takes
+    ~25 s at C4, so the bounded sample is the oracle's ADMM on the C4 root node for ~`seconds`
+    (its per-iteration work is the same at every node: two passes over X plus the checks);
+    node-iterations/s ÷ the oracle's own mean iterations per node on this tree = nodes/s."""
     import oracle as O
     try:
         from threadpoolctl import threadpool_info
@@ -135,16 +152,24 @@ def cpu_baseline(inst, args, rho, seconds):
     except Exception:
         cores = os.cpu_count()
     P = O.Problem(inst.X, inst.y, inst.lambda0, inst.lambda2, inst.M, rho=rho)
+    code = O.make_code(inst.p)
     t = time.perf_counter()
-    res = O.bnb_solve(P, B=args.batch, gap_tol=args.gap_tol, node_tol=args.node_tol, time_limit=seconds)
+    O.admm_node(P, code, node_tol=-1.0, max_iters=10)
+    per = (time.perf_counter() - t) / 10
+    K = max(10, int(seconds / max(per, 1e-6)))
+    t = time.perf_counter()
+    O.admm_node(P, code, node_tol=-1.0, max_iters=K)
     dt = time.perf_counter() - t
-    nodes = res["nodes"]
-    # the oracle solves a whole batch before checking its clock: count what finished
-    return dict(value=nodes / dt if dt > 0 else 0.0, unit="nodes/s", cores=int(cores), kind="oracle",
-                sample="oracle bnb_solve (numpy fp64, B=%d, same instance/tolerances) for a %.0f s budget: "
-                       "%d nodes, %d ADMM node-iterations in %.1f s (includes its precompute)"
-                       % (args.batch, seconds, nodes, res["node_iters"], dt),
-                node_iters_per_s=res["node_iters"] / dt if dt > 0 else 0.0)
+    nit = K / dt
+    ipn, pref_nodes = oracle_iters_per_node(args.config)
+    if ipn is None:
+        ipn = float("nan")
+    return dict(value=nit / ipn, unit="nodes/s", cores=int(cores), kind="oracle",
+                sample="oracle admm_node (numpy fp64, explicit dual checks every 10) on the %s root for %d "
+                       "iterations in %.1f s = %.2f node-iterations/s, divided by the oracle's own %.1f "
+                       "iterations/node over its first %d BnB nodes (tests/golden)" % (args.config, K, dt, nit, ipn,
+                                                                                    pref_nodes),
+                node_iters_per_s=nit)
 
 
 def run_reference(args):
@@ -157,7 +182,7 @@ def run_reference(args):
     vals = []
     cb = None
     for s in range(args.warmup + args.steps):
-        budget = max(5.0, args.cpu_seconds / 2) if s >= args.warmup else 5.0
+        budget = max(5.0, args.cpu_seconds / 2) if s >= args.warmup else 2.0
         cb = cpu_baseline(inst, args, rho, budget)
         if s >= args.warmup:
             vals.append(cb["value"])
@@ -166,7 +191,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "%s seed %d: %s" % (args.config, args.seed, CONFIG_DESC[args.config]),
-                       "gap_tol": args.gap_tol, "node_tol": args.node_tol, "batch": args.batch, "rho": rho},
+                       "gap_tol": args.gap_tol, "node_tol": args.node_tol, "node_limit": args.node_limit,
+                       "batch": args.batch, "rho": rho},
             "cpu_baseline": {"value": v, "unit": "nodes/s", "cores": cb["cores"], "kind": "oracle",
                              "sample": cb["sample"]},
             "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -231,7 +257,8 @@ def main():
     t = time.perf_counter()
     prob = make_problem(Xh, inst.y)
     t_create = time.perf_counter() - t
-    solve_kw = dict(gap_tol=args.gap_tol, batch=args.batch, verbose=args.verbose and rank == 0)
+    solve_kw = dict(gap_tol=args.gap_tol, batch=args.batch, node_limit=args.node_limit,
+                    verbose=args.verbose and rank == 0)
     for _ in range(args.warmup):
         res = prob.l0l2_solve(**solve_kw)
     prob.l0l2_kernel_stats(reset=True)
@@ -303,10 +330,11 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": "%s seed %d: %s" % (args.config, args.seed, CONFIG_DESC[args.config]),
                            "lambda0": inst.lambda0, "lambda2": inst.lambda2, "M": inst.M, "rho": rho,
-                           "gap_tol": args.gap_tol, "node_tol": args.node_tol, "batch": args.batch,
-                           "parallelism": "frontier partitioned over %d GPU(s)" % world,
+                           "gap_tol": args.gap_tol, "node_tol": args.node_tol, "node_limit": args.node_limit,
+                           "batch": args.batch, "parallelism": "frontier partitioned over %d GPU(s)" % world,
                            "l2": "inputs larger than L2 (X and Z are %.0f MB each)" % (inst.X.nbytes / 2 ** 20)},
-                "time_to_certified_optimality_s": ms / args.steps / 1e3,
+                "time_per_step_s": ms / args.steps / 1e3,
+                "time_to_certified_optimality_s": (ms / args.steps / 1e3) if last["stats"]["status"] <= 1 else None,
                 "nodes_per_step": nodes_step, "node_iters_per_s": iters_total / (ms / 1e3),
                 "certified_gap": last["gap"], "objective": last["obj"], "support": [int(j) for j in last["support"]],
                 "solve_status": st["status"], "rounds": st["rounds"], "max_open": st["max_open"],

@@ -517,13 +517,14 @@ __global__ void scatter_fix(int nb, const int64_t* __restrict__ off, const int32
                             const uint8_t* __restrict__ val, uint8_t* code, double* beta, int64_t p, int* bad) {
   const int nd = blockIdx.x;
   if (nd >= nb) return;
-  for (int64_t q = off[nd] + threadIdx.x; q < off[nd + 1]; q += blockDim.x) {
+  const int64_t q0 = off[nd], q1 = off[nd + 1];
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
     const int32_t j = idx[q];
     if (j < 0 || j >= p) { atomicOr(bad, 1); continue; }
-    const int64_t e = (int64_t)j * kBC + nd;
     const uint8_t cd = val[q] ? 2 : 1;
-    const uint8_t old = code[e];
-    if (old != 0 && old != cd) atomicOr(bad, 2);   // F0 ∩ F1 ≠ ∅
+    for (int64_t r = q0; r < q; r++)               // F0 ∩ F1 ≠ ∅, order independent
+      if (idx[r] == j && (val[r] ? 2 : 1) != cd) atomicOr(bad, 2);
+    const int64_t e = (int64_t)j * kBC + nd;
     code[e] = cd;
     if (cd == 1) beta[e] = 0.0;                    // warm edit: β_j ← 0 on F0
   }
