@@ -30,7 +30,7 @@
 namespace l0l2 {
 namespace {
 
-constexpr int NW = kAdmmThreads / 32;   // 16 warps
+constexpr int NW = kAdmmThreads / 32;   // 16 warps: 14 MMA + 2 epilogue
 constexpr int F_ACTIVE = 8;             // internal node flag bit (not exported)
 
 struct KP {
@@ -159,15 +159,24 @@ constexpr int NST = 3;         // Z tile stages in the TMA ring
 constexpr int PFD = 3;         // additional tiles prefetched into L2 beyond the smem ring
 constexpr int NMW = NW - 2;    // MMA warps (adjoint + forward); the last 2 warps run the epilogue
 constexpr int MMA_THREADS = NMW * 32;
-constexpr int MAXKS = 26;      // adjoint k-steps (4 rows each) per MMA warp held in registers
-constexpr int MAXMT2 = 13;     // forward row tiles (8 rows) per MMA warp  → n ≤ 10·13·8 = 1040
+// n classes of the kernel: KS adjoint k-steps (4 rows) and MT forward row tiles (8 rows) per MMA
+// warp, so n8 ≤ min(4·NMW·KS, 8·NMW·MT).  (19, 10) is the largest: n ≤ 1064.
+constexpr int NCLS = 5;
+constexpr int CLS_KS[NCLS] = {2, 5, 10, 18, 19};
+constexpr int CLS_MT[NCLS] = {1, 3, 5, 9, 10};
 // named barriers (id 0 is __syncthreads)
 constexpr int BAR_ADJ = 1;     // +0/+1 (double buffered): MMA → epilogue "S_J partials ready"
 constexpr int BAR_EPI = 3;     // +0/+1: epilogue → MMA "w⁺_J ready"
 constexpr int BAR_MMA = 5;     // MMA warps only: "tile stage released"
 
+// Per-stage copy of the epilogue's operands for tile J, TMA'd with Z_J on the same mbarrier:
+//   β_J [8][8], v_J [8][8], c_J [8], code_J [8][8] bytes (node-minor, as in HBM)
+constexpr int STQ = 64 + 64 + 8 + 8;                       // doubles per stage
+constexpr unsigned STQ_BYTES = 512 + 512 + 64 + 64;
+
 struct Smem {
   double* tiles;      // [NST][kPt][ld]   Z_J ring (stage q at tiles + q·kPt·ld)
+  double* stq;        // [NST][STQ]       β_J, v_J, c_J, code_J of the staged tile
   double* spart;      // [2][NMW][64]     adjoint partials per MMA warp (double buffered)
   double* Ws;         // [2][kBC][12]     w⁺_J (node-major, padded; double buffered)
   double* red;        // [kBC]            running max of checked duals (R7)
@@ -188,6 +197,33 @@ __device__ __forceinline__ void nbar_arrive(int id, int cnt) {
 
 enum { SW_FWD_W = 0, SW_FWD_BETA = 1, SW_FUSED = 2 };
 
+__device__ __forceinline__ unsigned tile_bytes(const KP& k) { return (unsigned)(kPt * k.ld * sizeof(double)); }
+
+// stage t → ring slot sg: Z_J plus the epilogue operands of the same columns (one mbarrier)
+__device__ __forceinline__ void issue_stage(const KP& k, Smem& s, int t, int sg) {
+  const unsigned tb = tile_bytes(k);
+  mbar_expect_tx(&s.mbar[sg], tb + STQ_BYTES);
+  bulk_g2s(s.tiles + (size_t)sg * kPt * k.ld, k.Z + (int64_t)t * kPt * k.ld, tb, &s.mbar[sg]);
+  double* q = s.stq + sg * STQ;
+  bulk_g2s(q, k.beta + (int64_t)t * kPt * kBC, 512, &s.mbar[sg]);
+  bulk_g2s(q + 64, k.v + (int64_t)t * kPt * kBC, 512, &s.mbar[sg]);
+  bulk_g2s(q + 128, k.c + (int64_t)t * kPt, 64, &s.mbar[sg]);
+  bulk_g2s(q + 136, k.code + (int64_t)t * kPt * kBC, 64, &s.mbar[sg]);
+}
+
+// Fill the first NST ring slots of this CTA's tile range (and L2-prefetch PFD more).  Called by
+// thread 0 once before the first sweep and again at the end of every sweep, so the next sweep's
+// first tiles stream in while the grid reduces u (every sweep reads the same tile range).  The
+// β, v of those tiles were written by this CTA's epilogue threads, which fence the generic →
+// async proxy before the CTA barrier that precedes this call.
+__device__ void prefill(const KP& k, Smem& s) {
+  const int g = blockIdx.x, G = gridDim.x;
+  const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
+  fence_proxy_async_smem();
+  for (int t = t0; t < t1 && t < t0 + NST; t++) issue_stage(k, s, t, (t - t0) % NST);
+  for (int t = t0 + NST; t < t1 && t < t0 + NST + PFD; t++) prefetch_l2(k.Z + (int64_t)t * kPt * k.ld, tile_bytes(k));
+}
+
 // One sweep over this CTA's tiles, warp-specialised:
 //   MMA warps (0..NMW−1):  adj(t0); for t: [adj(t+1)] → wait w⁺(t) → fwd(t) → release stage(t)
 //   epilogue warps:        for t: wait S(t) → b, β⁺, v⁺, w⁺, check sums → publish w⁺(t)
@@ -195,55 +231,44 @@ enum { SW_FWD_W = 0, SW_FWD_BETA = 1, SW_FUSED = 2 };
 // iteration lives in registers as the adjoint's B fragments (MMA warp w owns k-steps [ks0, ks1),
 // lane holds U[row = 4q + lane%4][node = lane/4]).  Forward partials go to Upart[cta], check sums
 // to sums[cta].
-template <int MODE>
+template <int MODE, int KS, int MT>
 __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& phases) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.x, G = gridDim.x;
   const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
-  const unsigned tile_bytes = (unsigned)(kPt * k.ld * sizeof(double));
   constexpr bool fused = (MODE == SW_FUSED);
   const bool is_mma = warp < NMW;
 
   if (is_mma) {
+    // Branch-free fragment schedule (so every shared-memory fragment load can be hoisted ahead of
+    // its DMMA): warp w owns adjoint k-steps q = w + NMW·i (i < KS) and forward row tiles
+    // m = w + NMW·i (i < MT); indices past the end are clamped to a valid row (their u fragment is
+    // 0, their forward accumulator is never stored).
     const int mt = (int)(k.n8 / 8);
     const int kt = (int)(k.n8 / 4);
-    const int ks0 = kt * warp / NMW, ks1 = kt * (warp + 1) / NMW;
-    double acc[MAXMT2][2];
+    const int ld = (int)k.ld;
+    const int cA = lane >> 2, kA = lane & 3;
+    double acc[MT][2];
 #pragma unroll
-    for (int i = 0; i < MAXMT2; i++) acc[i][0] = acc[i][1] = 0.0;
-    double uf[MAXKS];
-    if (fused) {
+    for (int i = 0; i < MT; i++) acc[i][0] = acc[i][1] = 0.0;
+    double uf[KS];
 #pragma unroll
-      for (int qi = 0; qi < MAXKS; qi++) {
-        const int q = ks0 + qi;
-        uf[qi] = (q < ks1) ? __ldcg(k.U + (lane >> 2) * k.ld + q * 4 + (lane & 3)) : 0.0;
-      }
-    }
-    // prologue: fill NST stages, prefetch PFD more tiles into L2
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      for (int t = t0; t < t1 && t < t0 + NST; t++) {
-        const int sg = (t - t0) % NST;
-        mbar_expect_tx(&s.mbar[sg], tile_bytes);
-        bulk_g2s(s.tiles + (size_t)sg * kPt * k.ld, k.Z + (int64_t)t * kPt * k.ld, tile_bytes, &s.mbar[sg]);
-      }
-      for (int t = t0 + NST; t < t1 && t < t0 + NST + PFD; t++) prefetch_l2(k.Z + (int64_t)t * kPt * k.ld, tile_bytes);
+    for (int i = 0; i < KS; i++) {
+      const int q = warp + NMW * i;
+      uf[i] = (fused && q < kt) ? __ldcg(k.U + cA * ld + q * 4 + kA) : 0.0;
     }
     auto adjoint = [&](int t) {
       const int sg = (t - t0) % NST;
       mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
       phases ^= 1u << sg;
-      const double* T = s.tiles + (size_t)sg * kPt * k.ld;
-      double sc0[2] = {0.0, 0.0}, sc1[2] = {0.0, 0.0};
+      const double* T = s.tiles + (size_t)sg * kPt * ld + cA * ld + kA;
+      double sc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-      for (int qi = 0; qi < MAXKS; qi += 2) {
-        if (ks0 + qi < ks1) dmma(sc0, T[(lane >> 2) * k.ld + (ks0 + qi) * 4 + (lane & 3)], uf[qi]);
-        if (ks0 + qi + 1 < ks1) dmma(sc1, T[(lane >> 2) * k.ld + (ks0 + qi + 1) * 4 + (lane & 3)], uf[qi + 1]);
-      }
+      for (int i = 0; i < KS; i++) dmma(sc[i & 3], T[4 * min(warp + NMW * i, kt - 1)], uf[i]);
       double* sp = s.spart + ((t - t0) & 1) * NMW * 64 + warp * 64;
       // C fragment: row (col j) = lane>>2, cols (node) = 2*(lane&3) + {0,1}
-      sp[(lane >> 2) * 8 + 2 * (lane & 3)] = sc0[0] + sc1[0];
-      sp[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = sc0[1] + sc1[1];
+      sp[cA * 8 + 2 * kA] = (sc[0][0] + sc[1][0]) + (sc[2][0] + sc[3][0]);
+      sp[cA * 8 + 2 * kA + 1] = (sc[0][1] + sc[1][1]) + (sc[2][1] + sc[3][1]);
       nbar_arrive(BAR_ADJ + ((t - t0) & 1), kAdmmThreads);
     };
     if (fused && t0 < t1) adjoint(t0);
@@ -259,34 +284,30 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
         phases ^= 1u << sg;
       }
       nbar_sync(BAR_EPI + ((t - t0) & 1), kAdmmThreads);   // w⁺_J(t) published
-      const double* T = s.tiles + (size_t)sg * kPt * k.ld;
+      const double* T = s.tiles + (size_t)sg * kPt * ld + kA * ld + cA;
       const double* W = s.Ws + ((t - t0) & 1) * kBC * 12;
       // ---- forward: U⁺(rows × 8 nodes) += Z_J (rows × 8 cols) · W_J (8 cols × 8 nodes)
-      const double b0 = W[(lane >> 2) * 12 + (lane & 3)];         // B[k = j][n = node]
-      const double b1 = W[(lane >> 2) * 12 + 4 + (lane & 3)];
+      const double b0 = W[cA * 12 + kA];         // B[k = j][n = node]
+      const double b1 = W[cA * 12 + 4 + kA];
 #pragma unroll
-      for (int i = 0; i < MAXMT2; i++) {
-        const int m = warp + i * NMW;
-        if (m < mt) {
-          const int row = m * 8 + (lane >> 2);
-          dmma(acc[i], T[(lane & 3) * k.ld + row], b0);            // A[m = row][k = col j]
-          dmma(acc[i], T[(4 + (lane & 3)) * k.ld + row], b1);
-        }
+      for (int i = 0; i < MT; i++) {
+        const int row = 8 * min(warp + NMW * i, mt - 1);
+        dmma(acc[i], T[row], b0);                // A[m = row][k = col j]
+        dmma(acc[i], T[4 * ld + row], b1);
       }
       if (!fused && t + 2 < t1) nbar_arrive(BAR_ADJ + ((t - t0) & 1), kAdmmThreads);   // w⁺ buffer free for t+2
       nbar_sync(BAR_MMA, MMA_THREADS);                             // every MMA warp is done with stage(t)
       if (tid == 0 && t + NST < t1) {
         fence_proxy_async_smem();
-        mbar_expect_tx(&s.mbar[sg], tile_bytes);
-        bulk_g2s(s.tiles + (size_t)sg * kPt * k.ld, k.Z + (int64_t)(t + NST) * kPt * k.ld, tile_bytes, &s.mbar[sg]);
-        if (t + NST + PFD < t1) prefetch_l2(k.Z + (int64_t)(t + NST + PFD) * kPt * k.ld, tile_bytes);
+        issue_stage(k, s, t + NST, sg);
+        if (t + NST + PFD < t1) prefetch_l2(k.Z + (int64_t)(t + NST + PFD) * kPt * k.ld, tile_bytes(k));
       }
       __syncwarp();
     }
     // ---- this CTA's forward partial: Upart[g][node][row]
     double* up = k.Upart + (int64_t)g * kBC * k.ld;
 #pragma unroll
-    for (int i = 0; i < MAXMT2; i++) {
+    for (int i = 0; i < MT; i++) {
       const int m = warp + i * NMW;
       if (m < mt) {
         const int row = m * 8 + (lane >> 2), nd = 2 * (lane & 3);
@@ -302,8 +323,12 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
     for (int t = t0; t < t1; t++) {
       const int64_t col0 = (int64_t)t * kPt;
       const int64_t e = (col0 + j) * kBC + nd;
-      const double st_beta = k.beta[e], st_v = k.v[e], st_c = k.c[col0 + j];
-      const uint8_t st_code = k.code[e];
+      const int sg = (t - t0) % NST;
+      mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);   // stage t landed (its state operands too)
+      phases ^= 1u << sg;
+      const double* q = s.stq + sg * STQ;
+      const double st_beta = q[et], st_v = q[64 + et], st_c = q[128 + j];
+      const uint8_t st_code = reinterpret_cast<const uint8_t*>(q + 136)[et];
       double wn = 0.0;
       // fused: S_J(t) partials written; forward-only: w⁺ buffer (t−t0)&1 released by the MMA warps
       nbar_sync(BAR_ADJ + ((t - t0) & 1), kAdmmThreads);
@@ -334,6 +359,8 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       s.Ws[((t - t0) & 1) * kBC * 12 + nd * 12 + j] = wn;
       nbar_arrive(BAR_EPI + ((t - t0) & 1), kAdmmThreads);
     }
+    // β, v were written through the generic proxy; the next sweep reads them with TMA
+    fence_proxy_async_global();
     if (fused && check) {
       // stash per-thread sums; reduced below after the CTA barrier
       s.Ws[2 * kBC * 12 + et * 4 + 0] = sT1;
@@ -343,6 +370,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
     }
   }
   __syncthreads();
+  if (tid == 0) prefill(k, s);
   if (fused && check && tid < kBC * 4) {
     const int nd = tid >> 2, q = tid & 3;
     double a = 0.0;
@@ -351,19 +379,38 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
   }
 }
 
-// Fixed-order grid reduction of the forward partials into dst[node][row] (rows < n8).
-__device__ void reduce_u(const KP& k, double* dst) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Fixed-order grid reduction of the forward partials into dst[node][row] (rows < n8).  CTA g owns
+// elements [e0, e1) (≤ RED_E of them per pass); thread (c, e) sums partials q ∈ chunk c in order,
+// then chunk sums are added in chunk order — deterministic and independent of the batch.
+constexpr int RED_E = 64;
+constexpr int RED_C = kAdmmThreads / RED_E;
+__device__ void reduce_u(const KP& k, Smem& s, double* dst) {
+  const int tid = threadIdx.x;
   const int g = blockIdx.x, G = gridDim.x;
   const int64_t E = (int64_t)kBC * k.n8;
   const int64_t e0 = E * g / G, e1 = E * (g + 1) / G;
-  for (int64_t e = e0 + warp; e < e1; e += NW) {
-    const int64_t nd = e / k.n8, row = e % k.n8;
+  const int el = tid % RED_E, c = tid / RED_E;
+  const int q0 = G * c / RED_C, q1 = G * (c + 1) / RED_C;
+  for (int64_t eb = e0; eb < e1; eb += RED_E) {
+    const int64_t e = eb + el;
     double a = 0.0;
-    for (int q = lane; q < G; q += 32) a += __ldcg(k.Upart + ((int64_t)q * kBC + nd) * k.ld + row);
+    if (e < e1) {
+      const int64_t nd = e / k.n8, row = e % k.n8;
+      const double* src = k.Upart + nd * k.ld + row;
+      const int64_t qs = (int64_t)kBC * k.ld;
+#pragma unroll 8
+      for (int q = q0; q < q1; q++) a += __ldcg(src + q * qs);
+    }
+    s.spart[c * RED_E + el] = a;
+    __syncthreads();
+    if (c == 0 && e < e1) {
+      double r = s.spart[el];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) dst[nd * k.ld + row] = a;
+      for (int cc = 1; cc < RED_C; cc++) r += s.spart[cc * RED_E + el];
+      const int64_t nd = e / k.n8, row = e % k.n8;
+      dst[nd * k.ld + row] = r;
+    }
+    __syncthreads();
   }
 }
 
@@ -403,13 +450,15 @@ __device__ void lmatvec_partial(const KP& k, Smem& s) {
   }
 }
 
+template <int KS, int MT>
 __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem s;
   {
     double* base = reinterpret_cast<double*>(smem_raw);
     s.tiles = base;
-    s.spart = base + (size_t)NST * kPt * k.ld;
+    s.stq = base + (size_t)NST * kPt * k.ld;
+    s.spart = s.stq + NST * STQ;
     s.Ws = s.spart + 2 * NMW * 64;
     s.red = s.Ws + 2 * kBC * 12 + 64 * 4;
     s.mbar = reinterpret_cast<uint64_t*>(s.red + kBC);
@@ -426,27 +475,28 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   }
   __syncthreads();
   unsigned phases = 0;
+  if (tid == 0) prefill(k, s);
 
   // u0 = Z (c + ρβ0 − v0), then the warm/cold refresh sweep (R6)
-  sweep<SW_FWD_W>(k, s, false, false, phases);
+  sweep<SW_FWD_W, KS, MT>(k, s, false, false, phases);
   grid_sync(k.bar);
-  reduce_u(k, k.U);
+  reduce_u(k, s, k.U);
   grid_sync(k.bar);
-  sweep<SW_FUSED>(k, s, true, false, phases);
+  sweep<SW_FUSED, KS, MT>(k, s, true, false, phases);
   grid_sync(k.bar);
-  reduce_u(k, k.U);
+  reduce_u(k, s, k.U);
   grid_sync(k.bar);
 
   for (int it = 1; it <= k.max_iters; it++) {
     const bool chk = (it % k.check_every == 0) || (it == k.max_iters);
-    sweep<SW_FUSED>(k, s, false, chk, phases);
+    sweep<SW_FUSED, KS, MT>(k, s, false, chk, phases);
     grid_sync(k.bar);
-    reduce_u(k, k.U);
+    reduce_u(k, s, k.U);
     grid_sync(k.bar);
     if (!chk) continue;
-    sweep<SW_FWD_BETA>(k, s, false, false, phases);
+    sweep<SW_FWD_BETA, KS, MT>(k, s, false, false, phases);
     grid_sync(k.bar);
-    reduce_u(k, k.Ub);
+    reduce_u(k, s, k.Ub);
     grid_sync(k.bar);
     lmatvec_partial(k, s);
     grid_sync(k.bar);
@@ -482,6 +532,12 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     int any = 0;
     for (int nd = 0; nd < kBC; nd++) any |= s.flags[nd] & F_ACTIVE;
     if (!any) break;
+  }
+  // drain the prefill issued after the last sweep before the CTA retires
+  if (tid == 0) {
+    const int g = blockIdx.x, G = gridDim.x;
+    const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
+    for (int sg = 0; sg < NST && t0 + sg < t1; sg++) mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
   }
   if (blockIdx.x == 0 && tid < k.nb) {
     const int nd = tid;
@@ -634,17 +690,35 @@ __global__ void fill_y(double* r, int64_t ldr, const double* y, int64_t n, int n
   r[(e / n) * ldr + e % n] = y[e % n];
 }
 
+using AdmmKernel = void (*)(KP);
+AdmmKernel admm_kernel(int cls) {
+  switch (cls) {
+    case 0: return admm_persistent<CLS_KS[0], CLS_MT[0]>;
+    case 1: return admm_persistent<CLS_KS[1], CLS_MT[1]>;
+    case 2: return admm_persistent<CLS_KS[2], CLS_MT[2]>;
+    case 3: return admm_persistent<CLS_KS[3], CLS_MT[3]>;
+    default: return admm_persistent<CLS_KS[4], CLS_MT[4]>;
+  }
+}
+int admm_class(int64_t n8) {
+  for (int c = 0; c < NCLS; c++)
+    if (n8 <= 4 * NMW * CLS_KS[c] && n8 <= 8 * NMW * CLS_MT[c]) return c;
+  return -1;
+}
+
 }  // namespace
 
 size_t admm_smem_bytes(int64_t ld) {
-  return sizeof(double) * ((size_t)NST * kPt * ld + 2 * NMW * 64 + 2 * kBC * 12 + 64 * 4 + kBC) +
+  return sizeof(double) * ((size_t)NST * kPt * ld + NST * STQ + 2 * NMW * 64 + 2 * kBC * 12 + 64 * 4 + kBC) +
          NST * sizeof(uint64_t) + kBC * sizeof(int) + 64;
 }
 
 int admm_alloc(Ctx* c) {
   const int64_t p8 = round8(c->p), ld = c->ld;
-  if (round8(c->n) / 8 > NMW * MAXMT2 || round8(c->n) / 4 > NMW * MAXKS)
-    return set_err(c, L0L2_EINVAL, "n = %lld > %d not supported by the fused ADMM kernel", (long long)c->n, NMW * MAXMT2 * 8);
+  c->admm_cls = admm_class(round8(c->n));
+  if (c->admm_cls < 0)
+    return set_err(c, L0L2_EINVAL, "n = %lld > %d not supported by the fused ADMM kernel", (long long)c->n,
+                   std::min(4 * NMW * CLS_KS[NCLS - 1], 8 * NMW * CLS_MT[NCLS - 1]));
   const int ntiles = (int)(p8 / kPt);
   c->grid = std::min(c->sms, ntiles);
   if (const char* e = getenv("L0L2_GRID")) c->grid = std::max(1, std::min(c->grid, atoi(e)));   // testing hook
@@ -670,9 +744,10 @@ int admm_alloc(Ctx* c) {
   L0L2_CUDA(c, cudaMemset(c->bchk, 0, sizeof(double) * p8 * kBC));
   L0L2_CUDA(c, cudaMemset(c->bar, 0, sizeof(unsigned) * 2));
   const size_t smem = admm_smem_bytes(ld);
-  L0L2_CUDA(c, cudaFuncSetAttribute(admm_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const AdmmKernel kern = admm_kernel(c->admm_cls);
+  L0L2_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int nblk = 0;
-  L0L2_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, admm_persistent, kAdmmThreads, smem));
+  L0L2_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, kern, kAdmmThreads, smem));
   if (nblk < 1) return set_err(c, L0L2_EINVAL, "ADMM kernel does not fit an SM (n=%lld)", (long long)c->n);
   return L0L2_OK;
 }
@@ -721,7 +796,7 @@ int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st) {
     for (auto& e : c->ev) L0L2_CUDA(c, cudaEventCreate(&e));
   }
   L0L2_CUDA(c, cudaEventRecord(c->ev[0], st));
-  L0L2_CUDA(c, cudaLaunchCooperativeKernel((void*)admm_persistent, dim3(c->grid), dim3(kAdmmThreads), args,
+  L0L2_CUDA(c, cudaLaunchCooperativeKernel((void*)admm_kernel(c->admm_cls), dim3(c->grid), dim3(kAdmmThreads), args,
                                            admm_smem_bytes(c->ld), st));
   L0L2_LAUNCHED(c);
   L0L2_CUDA(c, cudaEventRecord(c->ev[1], st));

@@ -12,7 +12,7 @@ namespace l0l2 {
 
 constexpr int kBC = 8;          // node columns per ADMM pass (DMMA n-dim = 8)
 constexpr int kPt = 8;          // Z columns per tile (DMMA m-dim of the adjoint = 8)
-constexpr int kAdmmThreads = 384;  // 12 warps per persistent CTA
+constexpr int kAdmmThreads = 512;  // 16 warps per persistent CTA
 constexpr int kSums = 6;        // per-node partial sums of a check (see admm.cu)
 
 // leading dimension of Z / X in HBM: ≥ n, even, ≡ 4 (mod 16) doubles so that the 8-byte
@@ -53,6 +53,7 @@ struct Ctx {
   void* ub_scratch = nullptr;                               // Gram spill for very large supports
   size_t ub_scratch_bytes = 0;
   int grid = 0;
+  int admm_cls = -1;                                        // n class of the ADMM kernel (admm.cu)
   // scratch for batch I/O in solve (device)
   std::vector<void*> owned;
   int64_t bytes = 0;
