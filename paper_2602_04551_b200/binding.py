@@ -7,7 +7,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(HERE, "libl0l2.so")
+_LIB_PATH = os.path.join(HERE, os.environ.get("L0L2_LIB", "libl0l2.so"))   # L0L2_LIB: in-tree variant (tuning runs)
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL = 0, -1, -2, -3, -4
 WNOTCONV, WLIMIT = 1, 2

@@ -31,6 +31,7 @@ namespace l0l2 {
 namespace {
 
 constexpr int NW = kAdmmThreads / 32;   // 16 warps: 14 MMA + 2 epilogue
+constexpr int NEW = 2;                  // epilogue warps
 constexpr int F_ACTIVE = 8;             // internal node flag bit (not exported)
 
 struct KP {
@@ -164,10 +165,6 @@ constexpr int MMA_THREADS = NMW * 32;
 constexpr int NCLS = 5;
 constexpr int CLS_KS[NCLS] = {2, 5, 10, 18, 19};
 constexpr int CLS_MT[NCLS] = {1, 3, 5, 9, 10};
-// named barriers (id 0 is __syncthreads)
-constexpr int BAR_ADJ = 1;     // +0/+1 (double buffered): MMA → epilogue "S_J partials ready"
-constexpr int BAR_EPI = 3;     // +0/+1: epilogue → MMA "w⁺_J ready"
-constexpr int BAR_MMA = 5;     // MMA warps only: "tile stage released"
 
 // Per-stage copy of the epilogue's operands for tile J, TMA'd with Z_J on the same mbarrier:
 //   β_J [8][8], v_J [8][8], c_J [8], code_J [8][8] bytes (node-minor, as in HBM)
@@ -181,21 +178,34 @@ struct Smem {
   double* Ws;         // [2][kBC][12]     w⁺_J (node-major, padded; double buffered)
   double* red;        // [kBC]            running max of checked duals (R7)
   uint64_t* mbar;     // [NST]
+  uint64_t* sready;   // [2]              S_J partials ready / w⁺ buffer free (NMW arrivals)
+  uint64_t* wready;   // [2]              w⁺_J ready (NEW arrivals)
   int* flags;         // [kBC]
+  unsigned* rel;      // [NST] MMA warps done with the stage (last one refills it)
 };
 
-// Named barriers.  The warp is re-converged first: lane 0 of MMA warp 0 diverges to issue TMA
-// refills, and the .aligned forms (bar.sync / bar.arrive) require a converged warp.
-__device__ __forceinline__ void nbar_sync(int id, int cnt) {
-  __syncwarp();
-  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void nbar_arrive(int id, int cnt) {
-  __syncwarp();
-  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+// Producer → consumer hand-offs inside the CTA are mbarriers, not named barriers: a named barrier
+// holding all MMA warps would also make every MMA warp wait for the slowest one each tile.
+//   sready[par]: MMA warps → epilogue "S_J partials of tile t written" (one arrival per MMA warp;
+//                in forward-only sweeps: "w⁺ buffer par free")
+//   wready[par]: epilogue → MMA warps "w⁺_J(t) written" (one arrival per epilogue warp)
+__device__ __forceinline__ void mbar_arrive_warp(uint64_t* b) {
+  __syncwarp();   // orders the lanes' shared-memory writes before lane 0's release-arrive
+  if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
 }
 
 enum { SW_FWD_W = 0, SW_FWD_BETA = 1, SW_FUSED = 2 };
+
+// Developer instrumentation (-DL0L2_PROF): per-warp clock64 totals of each wait / work phase,
+// read back with l0l2_debug_prof (tools/prof_phases.py).  Compiled out otherwise.
+#ifdef L0L2_PROF
+__device__ unsigned long long g_prof[160][NW][8];
+#define PROF_T0() long long pt_ = clock64()
+#define PROF_ACC(slot) do { long long n_ = clock64(); if ((threadIdx.x & 31) == 0) g_prof[blockIdx.x][threadIdx.x >> 5][slot] += (unsigned long long)(n_ - pt_); pt_ = n_; } while (0)
+#else
+#define PROF_T0() do {} while (0)
+#define PROF_ACC(slot) do {} while (0)
+#endif
 
 __device__ __forceinline__ unsigned tile_bytes(const KP& k) { return (unsigned)(kPt * k.ld * sizeof(double)); }
 
@@ -232,7 +242,7 @@ __device__ void prefill(const KP& k, Smem& s) {
 // lane holds U[row = 4q + lane%4][node = lane/4]).  Forward partials go to Upart[cta], check sums
 // to sums[cta].
 template <int MODE, int KS, int MT>
-__device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& phases) {
+__device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& phases, unsigned& hph) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.x, G = gridDim.x;
   const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
@@ -259,7 +269,9 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
     }
     auto adjoint = [&](int t) {
       const int sg = (t - t0) % NST;
+      PROF_T0();
       mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
+      PROF_ACC(0);
       phases ^= 1u << sg;
       const double* T = s.tiles + (size_t)sg * kPt * ld + cA * ld + kA;
       double sc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
@@ -269,12 +281,13 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       // C fragment: row (col j) = lane>>2, cols (node) = 2*(lane&3) + {0,1}
       sp[cA * 8 + 2 * kA] = (sc[0][0] + sc[1][0]) + (sc[2][0] + sc[3][0]);
       sp[cA * 8 + 2 * kA + 1] = (sc[0][1] + sc[1][1]) + (sc[2][1] + sc[3][1]);
-      nbar_arrive(BAR_ADJ + ((t - t0) & 1), kAdmmThreads);
+      mbar_arrive_warp(&s.sready[(t - t0) & 1]);
+      PROF_ACC(1);
     };
     if (fused && t0 < t1) adjoint(t0);
     if (!fused) {   // grant the two w⁺ buffers to the epilogue warps (no adjoint to pace them)
-      if (t0 < t1) nbar_arrive(BAR_ADJ + 0, kAdmmThreads);
-      if (t0 + 1 < t1) nbar_arrive(BAR_ADJ + 1, kAdmmThreads);
+      if (t0 < t1) mbar_arrive_warp(&s.sready[0]);
+      if (t0 + 1 < t1) mbar_arrive_warp(&s.sready[1]);
     }
     for (int t = t0; t < t1; t++) {
       if (fused && t + 1 < t1) adjoint(t + 1);
@@ -283,7 +296,13 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
         mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
         phases ^= 1u << sg;
       }
-      nbar_sync(BAR_EPI + ((t - t0) & 1), kAdmmThreads);   // w⁺_J(t) published
+      PROF_T0();
+      {   // w⁺_J(t) published
+        const int par = (t - t0) & 1;
+        mbar_wait(&s.wready[par], (hph >> par) & 1u);
+        hph ^= 1u << par;
+      }
+      PROF_ACC(2);
       const double* T = s.tiles + (size_t)sg * kPt * ld + kA * ld + cA;
       const double* W = s.Ws + ((t - t0) & 1) * kBC * 12;
       // ---- forward: U⁺(rows × 8 nodes) += Z_J (rows × 8 cols) · W_J (8 cols × 8 nodes)
@@ -295,14 +314,21 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
         dmma(acc[i], T[row], b0);                // A[m = row][k = col j]
         dmma(acc[i], T[4 * ld + row], b1);
       }
-      if (!fused && t + 2 < t1) nbar_arrive(BAR_ADJ + ((t - t0) & 1), kAdmmThreads);   // w⁺ buffer free for t+2
-      nbar_sync(BAR_MMA, MMA_THREADS);                             // every MMA warp is done with stage(t)
-      if (tid == 0 && t + NST < t1) {
-        fence_proxy_async_smem();
-        issue_stage(k, s, t + NST, sg);
-        if (t + NST + PFD < t1) prefetch_l2(k.Z + (int64_t)(t + NST + PFD) * kPt * k.ld, tile_bytes(k));
+      PROF_ACC(3);
+      if (!fused && t + 2 < t1) mbar_arrive_warp(&s.sready[(t - t0) & 1]);   // w⁺ buffer free for t+2
+      // release stage(t): the last MMA warp to finish its forward refills the slot (no CTA barrier;
+      // relaxed: this warp's fragment loads of stage(t) completed before its DMMAs issued)
+      __syncwarp();
+      if (lane == 0 && atomicAdd(&s.rel[sg], 1u) == NMW - 1) {
+        s.rel[sg] = 0;
+        if (t + NST < t1) {
+          fence_proxy_async_smem();
+          issue_stage(k, s, t + NST, sg);
+          if (t + NST + PFD < t1) prefetch_l2(k.Z + (int64_t)(t + NST + PFD) * kPt * k.ld, tile_bytes(k));
+        }
       }
       __syncwarp();
+      PROF_ACC(4);
     }
     // ---- this CTA's forward partial: Upart[g][node][row]
     double* up = k.Upart + (int64_t)g * kBC * k.ld;
@@ -324,23 +350,37 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       const int64_t col0 = (int64_t)t * kPt;
       const int64_t e = (col0 + j) * kBC + nd;
       const int sg = (t - t0) % NST;
+      PROF_T0();
       mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);   // stage t landed (its state operands too)
+      PROF_ACC(0);
       phases ^= 1u << sg;
       const double* q = s.stq + sg * STQ;
       const double st_beta = q[et], st_v = q[64 + et], st_c = q[128 + j];
       const uint8_t st_code = reinterpret_cast<const uint8_t*>(q + 136)[et];
+      // everything that does not depend on S_J is formed before the hand-off
+      const double w = st_c + k.rho * st_beta - st_v;      // eq:b_update input c + ρβ − v
+      const double vr = st_v * k.inv_rho;
       double wn = 0.0;
+      if (!fused && active) wn = (MODE == SW_FWD_BETA) ? st_beta : w;
       // fused: S_J(t) partials written; forward-only: w⁺ buffer (t−t0)&1 released by the MMA warps
-      nbar_sync(BAR_ADJ + ((t - t0) & 1), kAdmmThreads);
+      PROF_ACC(1);
+      mbar_wait(&s.sready[(t - t0) & 1], (hph >> ((t - t0) & 1)) & 1u);
+      hph ^= 1u << ((t - t0) & 1);
+      PROF_ACC(2);
       if (fused) {
-        const double* sp = s.spart + ((t - t0) & 1) * NMW * 64;
-        double sv = 0.0;
+        // S_J = Σ over the NMW k-split partials, pairwise in a fixed tree (short dependency chain)
+        const double* sp = s.spart + ((t - t0) & 1) * NMW * 64 + j * 8 + nd;
+        double part[NMW];
 #pragma unroll
-        for (int w = 0; w < NMW; w++) sv += sp[w * 64 + j * 8 + nd];   // fixed order
+        for (int i = 0; i < NMW; i++) part[i] = sp[i * 64];
+#pragma unroll
+        for (int h = 1; h < NMW; h *= 2)
+#pragma unroll
+          for (int i = 0; i + h < NMW; i += 2 * h) part[i] += part[i + h];
+        const double sv = part[0];
         if (active) {
-          const double w = st_c + k.rho * st_beta - st_v;
-          const double b = (w - sv) * k.inv_rho;
-          const double bn = refresh ? st_beta : prox(k, b + st_v * k.inv_rho, st_code);
+          const double b = (w - sv) * k.inv_rho;               // b = D w, D = (I − ZᵀZ)/ρ (R1)
+          const double bn = refresh ? st_beta : prox(k, b + vr, st_code);
           const double vn = st_v + k.rho * (b - bn);
           if (check) {
             sT1 = fma(b, sv, sT1);
@@ -353,11 +393,10 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
           k.v[e] = vn;
           wn = st_c + k.rho * bn - vn;
         }
-      } else if (active) {
-        wn = (MODE == SW_FWD_BETA) ? st_beta : st_c + k.rho * st_beta - st_v;
       }
       s.Ws[((t - t0) & 1) * kBC * 12 + nd * 12 + j] = wn;
-      nbar_arrive(BAR_EPI + ((t - t0) & 1), kAdmmThreads);
+      mbar_arrive_warp(&s.wready[(t - t0) & 1]);
+      PROF_ACC(5);
     }
     // β, v were written through the generic proxy; the next sweep reads them with TMA
     fence_proxy_async_global();
@@ -462,39 +501,50 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     s.Ws = s.spart + 2 * NMW * 64;
     s.red = s.Ws + 2 * kBC * 12 + 64 * 4;
     s.mbar = reinterpret_cast<uint64_t*>(s.red + kBC);
-    s.flags = reinterpret_cast<int*>(s.mbar + NST);
+    s.sready = s.mbar + NST;
+    s.wready = s.sready + 2;
+    s.flags = reinterpret_cast<int*>(s.wready + 2);
+    s.rel = reinterpret_cast<unsigned*>(s.flags + kBC);
   }
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int q = 0; q < NST; q++) mbar_init(&s.mbar[q], 1);
+    for (int q = 0; q < 2; q++) {
+      mbar_init(&s.sready[q], NMW);
+      mbar_init(&s.wready[q], NEW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (tid < NST) s.rel[tid] = 0;
   if (tid < kBC) {
     s.flags[tid] = __ldcg(k.nodei + tid * 2);
     s.red[tid] = -INFINITY;
   }
   __syncthreads();
-  unsigned phases = 0;
+  unsigned phases = 0, hph = 0;
   if (tid == 0) prefill(k, s);
 
   // u0 = Z (c + ρβ0 − v0), then the warm/cold refresh sweep (R6)
-  sweep<SW_FWD_W, KS, MT>(k, s, false, false, phases);
+  sweep<SW_FWD_W, KS, MT>(k, s, false, false, phases, hph);
   grid_sync(k.bar);
   reduce_u(k, s, k.U);
   grid_sync(k.bar);
-  sweep<SW_FUSED, KS, MT>(k, s, true, false, phases);
+  sweep<SW_FUSED, KS, MT>(k, s, true, false, phases, hph);
   grid_sync(k.bar);
   reduce_u(k, s, k.U);
   grid_sync(k.bar);
 
   for (int it = 1; it <= k.max_iters; it++) {
     const bool chk = (it % k.check_every == 0) || (it == k.max_iters);
-    sweep<SW_FUSED, KS, MT>(k, s, false, chk, phases);
+    PROF_T0();
+    sweep<SW_FUSED, KS, MT>(k, s, false, chk, phases, hph);
+    PROF_ACC(6);
     grid_sync(k.bar);
     reduce_u(k, s, k.U);
     grid_sync(k.bar);
+    PROF_ACC(7);
     if (!chk) continue;
-    sweep<SW_FWD_BETA, KS, MT>(k, s, false, false, phases);
+    sweep<SW_FWD_BETA, KS, MT>(k, s, false, false, phases, hph);
     grid_sync(k.bar);
     reduce_u(k, s, k.Ub);
     grid_sync(k.bar);
@@ -708,9 +758,22 @@ int admm_class(int64_t n8) {
 
 }  // namespace
 
+#ifdef L0L2_PROF
+int debug_prof(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_prof, sizeof(g_prof));
+  if (reset) {
+    static unsigned long long zero[160][NW][8];
+    cudaMemcpyToSymbol(g_prof, zero, sizeof(g_prof));
+  }
+  return (int)(sizeof(g_prof) / sizeof(unsigned long long));
+}
+#else
+int debug_prof(unsigned long long*, int) { return 0; }
+#endif
+
 size_t admm_smem_bytes(int64_t ld) {
   return sizeof(double) * ((size_t)NST * kPt * ld + NST * STQ + 2 * NMW * 64 + 2 * kBC * 12 + 64 * 4 + kBC) +
-         NST * sizeof(uint64_t) + kBC * sizeof(int) + 64;
+         (NST + 4) * sizeof(uint64_t) + kBC * sizeof(int) + NST * sizeof(unsigned) + 64;
 }
 
 int admm_alloc(Ctx* c) {

@@ -246,6 +246,9 @@ int l0l2_bound_batch(l0l2_ctx* ctx, int32_t B, const int64_t* fix_off, const int
   return notconv ? L0L2_WNOTCONV : L0L2_OK;
 }
 
+// developer instrumentation (only populated in -DL0L2_PROF builds; not part of include/l0l2.h)
+int l0l2_debug_prof(unsigned long long* out, int32_t reset) { return debug_prof(out, reset); }
+
 int l0l2_kernel_stats(l0l2_ctx* ctx, l0l2_kstats* out, int32_t reset) {
   if (!ctx) return L0L2_EINVAL;
   Ctx* c = &ctx->impl;

@@ -86,6 +86,7 @@ struct Ctx {
 };
 
 int set_err(Ctx* c, int code, const char* fmt, ...);
+int debug_prof(unsigned long long* out, int reset);   // -DL0L2_PROF builds only (admm.cu)
 void* dalloc(Ctx* c, size_t bytes);   // tracked cudaMalloc (nullptr on failure)
 
 #define L0L2_CUDA(ctx, expr)                                                            \
