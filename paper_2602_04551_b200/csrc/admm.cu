@@ -41,12 +41,19 @@ struct KP {
   double* beta; double* v; double* bchk;
   const uint8_t* __restrict__ code;
   double* U; double* Ub; double* Upart; double* sums; double* sums2;
+  // nonzeros of β⁺ at check iterations (sparse primal): per-CTA segments in tile
+  // order, then a dense per-node list in CTA order
+  int32_t* seg_idx; double* seg_val; int* seg_cnt;   // [grid][kBC][seg_cap], [grid][kBC]
+  int32_t* nz_idx; double* nz_val;                     // [kBC][nz_cap]
+  const double* __restrict__ X;                        // column-major, ld
+  int seg_cap, nz_cap;
   double* nodef;                   // [kBC][4]: lb_best, primal, parent_lb, last dual
   int* nodei;                      // [kBC][2]: flags, iters
   unsigned* bar;                   // [2]: count, generation
   double* out_lb; double* out_primal; int* out_iters; uint8_t* out_flags;
   int64_t ld, n, n8, p8;
-  int ntiles, nb, check_every, max_iters;
+  int ntiles, nb, check_every, max_iters, pfd;
+  int pfs;                         // tiles L2-prefetched by prefill (during the grid reduction)
   double rho, inv_rho, lam0, lam2, M, yy, node_tol;
   double shrink, sr, a_l1, a_4, psi_l1, psi_4, zsr;
   bool sr_le_M;
@@ -157,7 +164,7 @@ __device__ __forceinline__ double nu_f(const KP& k, double x, uint8_t code) {   
 
 // ---------------------------------------------------------------- shared memory layout
 constexpr int NST = 3;         // Z tile stages in the TMA ring
-constexpr int PFD = 3;         // additional tiles prefetched into L2 beyond the smem ring
+constexpr int PFD_DEFAULT = 1; // additional tiles prefetched into L2 beyond the smem ring (k.pfd)
 constexpr int NMW = NW - 2;    // MMA warps (adjoint + forward); the last 2 warps run the epilogue
 constexpr int MMA_THREADS = NMW * 32;
 // n classes of the kernel: KS adjoint k-steps (4 rows) and MT forward row tiles (8 rows) per MMA
@@ -182,6 +189,9 @@ struct Smem {
   uint64_t* wready;   // [2]              w⁺_J ready (NEW arrivals)
   int* flags;         // [kBC]
   unsigned* rel;      // [NST] MMA warps done with the stage (last one refills it)
+  int* ncnt;          // [kBC]            per-node β⁺ nonzero totals at a check (lmatvec fallback)
+  int* stile;         // [NST]            tile held by each ring slot (−1: end of this CTA's sweep)
+  int* sched;         // [4]              sweep number, stages issued, tiles taken, done (issuer only)
 };
 
 // Producer → consumer hand-offs inside the CTA are mbarriers, not named barriers: a named barrier
@@ -201,9 +211,11 @@ enum { SW_FWD_W = 0, SW_FWD_BETA = 1, SW_FUSED = 2 };
 #ifdef L0L2_PROF
 __device__ unsigned long long g_prof[160][NW][8];
 #define PROF_T0() long long pt_ = clock64()
+#define PROF_RESET() pt_ = clock64()
 #define PROF_ACC(slot) do { long long n_ = clock64(); if ((threadIdx.x & 31) == 0) g_prof[blockIdx.x][threadIdx.x >> 5][slot] += (unsigned long long)(n_ - pt_); pt_ = n_; } while (0)
 #else
 #define PROF_T0() do {} while (0)
+#define PROF_RESET() do {} while (0)
 #define PROF_ACC(slot) do {} while (0)
 #endif
 
@@ -221,17 +233,47 @@ __device__ __forceinline__ void issue_stage(const KP& k, Smem& s, int t, int sg)
   bulk_g2s(q + 136, k.code + (int64_t)t * kPt * kBC, 64, &s.mbar[sg]);
 }
 
-// Fill the first NST ring slots of this CTA's tile range (and L2-prefetch PFD more).  Called by
-// thread 0 once before the first sweep and again at the end of every sweep, so the next sweep's
-// first tiles stream in while the grid reduces u (every sweep reads the same tile range).  The
-// β, v of those tiles were written by this CTA's epilogue threads, which fence the generic →
-// async proxy before the CTA barrier that precedes this call.
-__device__ void prefill(const KP& k, Smem& s) {
+// Tile scheduling.  Every sweep streams all tiles of Z once; CTA g owns the fixed contiguous
+// range [t0, t1) (bitwise deterministic, independent of the batch composition).  The stages a
+// CTA consumes are numbered m = 0, 1, ... in ring order (slot m % NST); one thread issues each
+// (issue_next).  After the CTA's last tile one end-marker stage (tile −1, a plain arrive, no
+// copy) is issued and consumers stop at it.  The tile id is written before the (release) arrive,
+// so every consumer reads it after its (acquire) wait on the stage's mbarrier.  (A dynamic,
+// grid-wide ticket schedule was measured and gave nothing: the sweep is bound by aggregate HBM
+// bandwidth, not by the slowest SM — DESIGN.md §4.)
+__device__ void issue_next(const KP& k, Smem& s) {
+  if (s.sched[3]) return;
   const int g = blockIdx.x, G = gridDim.x;
   const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
-  fence_proxy_async_smem();
-  for (int t = t0; t < t1 && t < t0 + NST; t++) issue_stage(k, s, t, (t - t0) % NST);
-  for (int t = t0 + NST; t < t1 && t < t0 + NST + PFD; t++) prefetch_l2(k.Z + (int64_t)t * kPt * k.ld, tile_bytes(k));
+  const int sg = s.sched[1] % NST;
+  const int tile = t0 + s.sched[2] < t1 ? t0 + s.sched[2] : -1;
+  s.stile[sg] = tile;
+  s.sched[1]++;
+  if (tile >= 0) {
+    s.sched[2]++;
+    fence_proxy_async_smem();
+    issue_stage(k, s, tile, sg);
+    if (k.pfd > 0 && tile + k.pfd < t1) prefetch_l2(k.Z + (int64_t)(tile + k.pfd) * kPt * k.ld, tile_bytes(k));
+  } else {
+    s.sched[3] = 1;
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(&s.mbar[sg])) : "memory");
+  }
+}
+
+// Start sweep number `sw`: issue its first NST stages.  Called by thread 0 once before the first
+// sweep and again at the end of every sweep, so the next sweep's first tiles stream in while the
+// grid reduces u.  The β, v of any tile were written by some CTA's epilogue threads in an earlier
+// sweep (generic → async proxy fence, then grid barrier) before a stage can read them.
+__device__ void prefill(const KP& k, Smem& s, int sw) {
+  s.sched[0] = sw;
+  s.sched[1] = 0;
+  s.sched[2] = 0;
+  s.sched[3] = 0;
+  for (int m = 0; m < NST; m++) issue_next(k, s);
+  // the grid reduction that follows leaves HBM idle: pull the sweep's next tiles into L2 meanwhile
+  const int g = blockIdx.x, G = gridDim.x;
+  const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
+  for (int t = t0 + NST + k.pfd; t < t1 && t < t0 + NST + k.pfs; t++) prefetch_l2(k.Z + (int64_t)t * kPt * k.ld, tile_bytes(k));
 }
 
 // One sweep over this CTA's tiles, warp-specialised:
@@ -244,10 +286,16 @@ __device__ void prefill(const KP& k, Smem& s) {
 template <int MODE, int KS, int MT>
 __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& phases, unsigned& hph) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = blockIdx.x, G = gridDim.x;
-  const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
+  const int g = blockIdx.x;
   constexpr bool fused = (MODE == SW_FUSED);
   const bool is_mma = warp < NMW;
+  // wait for ring stage m; returns its tile (−1: the CTA's sweep is over)
+  auto stage = [&](int m) {
+    const int sg = m % NST;
+    mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
+    phases ^= 1u << sg;
+    return s.stile[sg];
+  };
 
   if (is_mma) {
     // Branch-free fragment schedule (so every shared-memory fragment load can be hoisted ahead of
@@ -267,44 +315,34 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       const int q = warp + NMW * i;
       uf[i] = (fused && q < kt) ? __ldcg(k.U + cA * ld + q * 4 + kA) : 0.0;
     }
-    auto adjoint = [&](int t) {
-      const int sg = (t - t0) % NST;
+    // adjoint of stage m (fused sweeps); false at the end marker
+    auto adjoint = [&](int m) {
       PROF_T0();
-      mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
+      const int tile = stage(m);
       PROF_ACC(0);
-      phases ^= 1u << sg;
-      const double* T = s.tiles + (size_t)sg * kPt * ld + cA * ld + kA;
+      if (tile < 0) return false;
+      const double* T = s.tiles + (size_t)(m % NST) * kPt * ld + cA * ld + kA;
       double sc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
       for (int i = 0; i < KS; i++) dmma(sc[i & 3], T[4 * min(warp + NMW * i, kt - 1)], uf[i]);
-      double* sp = s.spart + ((t - t0) & 1) * NMW * 64 + warp * 64;
+      double* sp = s.spart + (m & 1) * NMW * 64 + warp * 64;
       // C fragment: row (col j) = lane>>2, cols (node) = 2*(lane&3) + {0,1}
       sp[cA * 8 + 2 * kA] = (sc[0][0] + sc[1][0]) + (sc[2][0] + sc[3][0]);
       sp[cA * 8 + 2 * kA + 1] = (sc[0][1] + sc[1][1]) + (sc[2][1] + sc[3][1]);
-      mbar_arrive_warp(&s.sready[(t - t0) & 1]);
+      mbar_arrive_warp(&s.sready[m & 1]);
       PROF_ACC(1);
+      return true;
     };
-    if (fused && t0 < t1) adjoint(t0);
-    if (!fused) {   // grant the two w⁺ buffers to the epilogue warps (no adjoint to pace them)
-      if (t0 < t1) mbar_arrive_warp(&s.sready[0]);
-      if (t0 + 1 < t1) mbar_arrive_warp(&s.sready[1]);
-    }
-    for (int t = t0; t < t1; t++) {
-      if (fused && t + 1 < t1) adjoint(t + 1);
-      const int sg = (t - t0) % NST;
-      if (!fused) {
-        mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
-        phases ^= 1u << sg;
-      }
+    bool cur = fused ? adjoint(0) : stage(0) >= 0;
+    for (int m = 0; cur; m++) {
+      const int sg = m % NST;
+      const bool nxt = fused ? adjoint(m + 1) : true;
       PROF_T0();
-      {   // w⁺_J(t) published
-        const int par = (t - t0) & 1;
-        mbar_wait(&s.wready[par], (hph >> par) & 1u);
-        hph ^= 1u << par;
-      }
+      mbar_wait(&s.wready[m & 1], (hph >> (m & 1)) & 1u);   // w⁺_J(m) published
+      hph ^= 1u << (m & 1);
       PROF_ACC(2);
       const double* T = s.tiles + (size_t)sg * kPt * ld + kA * ld + cA;
-      const double* W = s.Ws + ((t - t0) & 1) * kBC * 12;
+      const double* W = s.Ws + (m & 1) * kBC * 12;
       // ---- forward: U⁺(rows × 8 nodes) += Z_J (rows × 8 cols) · W_J (8 cols × 8 nodes)
       const double b0 = W[cA * 12 + kA];         // B[k = j][n = node]
       const double b1 = W[cA * 12 + 4 + kA];
@@ -315,20 +353,22 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
         dmma(acc[i], T[4 * ld + row], b1);
       }
       PROF_ACC(3);
-      if (!fused && t + 2 < t1) mbar_arrive_warp(&s.sready[(t - t0) & 1]);   // w⁺ buffer free for t+2
-      // release stage(t): the last MMA warp to finish its forward refills the slot (no CTA barrier;
-      // relaxed: this warp's fragment loads of stage(t) completed before its DMMAs issued)
+      if (!fused) mbar_arrive_warp(&s.sready[m & 1]);   // w⁺ buffer m&1 free again
+      // release stage m: the last MMA warp to finish its forward refills the slot (no CTA barrier;
+      // acq_rel orders the scheduler state between successive issuing lanes)
       __syncwarp();
-      if (lane == 0 && atomicAdd(&s.rel[sg], 1u) == NMW - 1) {
-        s.rel[sg] = 0;
-        if (t + NST < t1) {
-          fence_proxy_async_smem();
-          issue_stage(k, s, t + NST, sg);
-          if (t + NST + PFD < t1) prefetch_l2(k.Z + (int64_t)(t + NST + PFD) * kPt * k.ld, tile_bytes(k));
+      if (lane == 0) {
+        // acq_rel: orders the scheduler state (s.sched) between successive issuing lanes
+        unsigned old;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(saddr(&s.rel[sg])) : "memory");
+        if (old == NMW - 1) {
+          s.rel[sg] = 0;
+          issue_next(k, s);
         }
       }
       __syncwarp();
       PROF_ACC(4);
+      cur = fused ? nxt : stage(m + 1) >= 0;
     }
     // ---- this CTA's forward partial: Upart[g][node][row]
     double* up = k.Upart + (int64_t)g * kBC * k.ld;
@@ -346,14 +386,17 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
     const int et = tid - MMA_THREADS, j = et >> 3, nd = et & 7;
     const bool active = (s.flags[nd] & F_ACTIVE) != 0;
     double sT1 = 0.0, sT2 = 0.0, sT3 = 0.0, sT4 = 0.0;
-    for (int t = t0; t < t1; t++) {
-      const int64_t col0 = (int64_t)t * kPt;
-      const int64_t e = (col0 + j) * kBC + nd;
-      const int sg = (t - t0) % NST;
+    const int ew = et >> 5;   // epilogue warp: columns 4·ew .. 4·ew + 3 of each tile
+    int seg_n = 0;            // β⁺ nonzeros of (this CTA, warp ew, node nd) so far (check sweeps)
+    int m = 0;
+    for (;; m++) {
       PROF_T0();
-      mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);   // stage t landed (its state operands too)
+      const int tile = stage(m);   // stage m landed (its state operands too), or the end marker
       PROF_ACC(0);
-      phases ^= 1u << sg;
+      if (tile < 0) break;
+      const int sg = m % NST;
+      const int64_t col0 = (int64_t)tile * kPt;
+      const int64_t e = (col0 + j) * kBC + nd;
       const double* q = s.stq + sg * STQ;
       const double st_beta = q[et], st_v = q[64 + et], st_c = q[128 + j];
       const uint8_t st_code = reinterpret_cast<const uint8_t*>(q + 136)[et];
@@ -362,14 +405,16 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       const double vr = st_v * k.inv_rho;
       double wn = 0.0;
       if (!fused && active) wn = (MODE == SW_FWD_BETA) ? st_beta : w;
-      // fused: S_J(t) partials written; forward-only: w⁺ buffer (t−t0)&1 released by the MMA warps
       PROF_ACC(1);
-      mbar_wait(&s.sready[(t - t0) & 1], (hph >> ((t - t0) & 1)) & 1u);
-      hph ^= 1u << ((t - t0) & 1);
+      // fused: S_J(m) partials written; forward-only: w⁺ buffer m&1 released by fwd(m − 2)
+      if (fused || m >= 2) {
+        mbar_wait(&s.sready[m & 1], (hph >> (m & 1)) & 1u);
+        hph ^= 1u << (m & 1);
+      }
       PROF_ACC(2);
       if (fused) {
         // S_J = Σ over the NMW k-split partials, pairwise in a fixed tree (short dependency chain)
-        const double* sp = s.spart + ((t - t0) & 1) * NMW * 64 + j * 8 + nd;
+        const double* sp = s.spart + (m & 1) * NMW * 64 + j * 8 + nd;
         double part[NMW];
 #pragma unroll
         for (int i = 0; i < NMW; i++) part[i] = sp[i * 64];
@@ -378,6 +423,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
 #pragma unroll
           for (int i = 0; i + h < NMW; i += 2 * h) part[i] += part[i + h];
         const double sv = part[0];
+        double bnz = 0.0;
         if (active) {
           const double b = (w - sv) * k.inv_rho;               // b = D w, D = (I − ZᵀZ)/ρ (R1)
           const double bn = refresh ? st_beta : prox(k, b + vr, st_code);
@@ -392,14 +438,35 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
           k.beta[e] = bn;
           k.v[e] = vn;
           wn = st_c + k.rho * bn - vn;
+          bnz = bn;
+        }
+        if (check) {
+          // append this tile's nonzeros of β⁺ to the (CTA, epilogue warp, node) segment, in column
+          // order: ballot + popcount, no barrier (every lane of a node keeps the same running count)
+          const unsigned bal = __ballot_sync(0xffffffffu, bnz != 0.0);
+          const unsigned mnode = bal & (0x01010101u << nd);
+          if (bnz != 0.0) {
+            const int r = seg_n + __popc(mnode & ((1u << (tid & 31)) - 1u));
+            const int64_t o = ((int64_t)(blockIdx.x * NEW + ew) * kBC + nd) * k.seg_cap + r;
+            k.seg_idx[o] = (int32_t)(col0 + j);
+            k.seg_val[o] = bnz;
+          }
+          seg_n += __popc(mnode);
         }
       }
-      s.Ws[((t - t0) & 1) * kBC * 12 + nd * 12 + j] = wn;
-      mbar_arrive_warp(&s.wready[(t - t0) & 1]);
+      s.Ws[(m & 1) * kBC * 12 + nd * 12 + j] = wn;
+      mbar_arrive_warp(&s.wready[m & 1]);
       PROF_ACC(5);
     }
+    // forward-only sweeps: consume the buffer-free arrivals of the last two forwards
+    if (!fused)
+      for (int i = m >= 2 ? m - 2 : 0; i < m; i++) {
+        mbar_wait(&s.sready[i & 1], (hph >> (i & 1)) & 1u);
+        hph ^= 1u << (i & 1);
+      }
     // β, v were written through the generic proxy; the next sweep reads them with TMA
     fence_proxy_async_global();
+    if (fused && check && (et & 31) < kBC) k.seg_cnt[(blockIdx.x * NEW + ew) * kBC + nd] = seg_n;
     if (fused && check) {
       // stash per-thread sums; reduced below after the CTA barrier
       s.Ws[2 * kBC * 12 + et * 4 + 0] = sT1;
@@ -409,7 +476,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
     }
   }
   __syncthreads();
-  if (tid == 0) prefill(k, s);
+  if (tid == 0) prefill(k, s, s.sched[0] + 1);
   if (fused && check && tid < kBC * 4) {
     const int nd = tid >> 2, q = tid & 3;
     double a = 0.0;
@@ -453,7 +520,90 @@ __device__ void reduce_u(const KP& k, Smem& s, double* dst) {
   }
 }
 
-// ‖L (Zβ)‖² partials: rows of L split over CTAs; per node one partial per CTA.
+// Dense per-node list of β⁺'s nonzeros: CTA g copies its segment to offset Σ_{g'<g} cnt[g'].
+// Returns (in tot[nd], every CTA identically) the node's total count.
+__device__ void compact_nonzeros(const KP& k, int* tot) {
+  const int g = blockIdx.x, G = gridDim.x;
+  __shared__ int off_s[kBC];
+  if (threadIdx.x < kBC) {
+    const int nd = threadIdx.x;
+    int off = 0, all = 0;
+    for (int q = 0; q < G * NEW; q++) {   // segments in (CTA, epilogue warp) order
+      const int c = __ldcg(k.seg_cnt + q * kBC + nd);
+      if (q < g * NEW) off += c;
+      all += c;
+    }
+    off_s[nd] = off;
+    tot[nd] = all;
+  }
+  __syncthreads();
+  for (int w = 0; w < NEW; w++)
+    for (int nd = 0; nd < kBC; nd++) {
+      const int q = g * NEW + w;
+      const int c = __ldcg(k.seg_cnt + q * kBC + nd);
+      int off = off_s[nd];
+      for (int ww = 0; ww < w; ww++) off += __ldcg(k.seg_cnt + (g * NEW + ww) * kBC + nd);
+      const int64_t so = ((int64_t)q * kBC + nd) * k.seg_cap;
+      for (int r = threadIdx.x; r < c; r += blockDim.x)
+        if (off + r < k.nz_cap) {
+          k.nz_idx[(int64_t)nd * k.nz_cap + off + r] = __ldcg(k.seg_idx + so + r);
+          k.nz_val[(int64_t)nd * k.nz_cap + off + r] = __ldcg(k.seg_val + so + r);
+        }
+    }
+}
+
+// ‖Xβ‖² partials from the sparse β⁺ (nodes with ≤ nz_cap nonzeros): CTA g owns rows [i0, i1).
+// Warp pair (2·nd, 2·nd+1) serves node nd: lane l of the pair takes entries e ≡ l (mod 64) and
+// accumulates X[i, j_e]·β_e for 8 rows i at once (one contiguous 64-byte piece of column j_e);
+// the 64 slot sums are reduced by a fixed butterfly and a fixed pair order — deterministic and
+// independent of the batch.
+__device__ void gather_partial(const KP& k, Smem& s, const int* tot) {
+  const int g = blockIdx.x, G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = k.n * g / G, i1 = k.n * (g + 1) / G;
+  const int nd = warp >> 1, slot = (warp & 1) * 32 + lane;
+  double* red = s.spart;   // [kBC][2][8]
+  const bool use = nd < kBC && (s.flags[nd] & F_ACTIVE) && tot[nd] <= k.nz_cap;
+  double part = 0.0;
+  for (int64_t r0 = i0; r0 < i1; r0 += 8) {
+    double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (use) {
+      const int cnt = tot[nd];
+      const int32_t* ix = k.nz_idx + (int64_t)nd * k.nz_cap;
+      const double* vx = k.nz_val + (int64_t)nd * k.nz_cap;
+      const int nr = (int)(i1 - r0 < 8 ? i1 - r0 : 8);
+#pragma unroll 2
+      for (int e = slot; e < cnt; e += 64) {
+        const double bv = __ldcg(vx + e);
+        const double* col = k.X + (int64_t)__ldcg(ix + e) * k.ld + r0;
+#pragma unroll
+        for (int r = 0; r < 8; r++)
+          if (r < nr) a[r] = fma(bv, __ldg(col + r), a[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; r++)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a[r] += __shfl_xor_sync(0xffffffffu, a[r], o);
+    if (nd < kBC && lane < 8) {
+      double v = 0.0;
+#pragma unroll
+      for (int r = 0; r < 8; r++) v = lane == r ? a[r] : v;
+      red[(nd * 2 + (warp & 1)) * 8 + lane] = v;
+    }
+    __syncthreads();
+    if (tid < kBC) {
+      for (int r = 0; r < 8 && r0 + r < i1; r++) {
+        const double xb = red[(tid * 2) * 8 + r] + red[(tid * 2 + 1) * 8 + r];
+        part = fma(xb, xb, part);
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < kBC && (s.flags[tid] & F_ACTIVE) && tot[tid] <= k.nz_cap) k.sums2[(int64_t)g * kBC + tid] = part;
+}
+
+// ‖L (Zβ)‖² partials: rows of L split over CTAs; per node one partial per CTA (nodes whose β⁺
+// has more than nz_cap nonzeros; the others use gather_partial).
 __device__ void lmatvec_partial(const KP& k, Smem& s) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = blockIdx.x, G = gridDim.x;
@@ -482,7 +632,7 @@ __device__ void lmatvec_partial(const KP& k, Smem& s) {
   if (lane == 0)
     for (int nd = 0; nd < kBC; nd++) s.spart[warp * kBC + nd] = part[nd];
   __syncthreads();
-  if (threadIdx.x < kBC) {
+  if (threadIdx.x < kBC && s.ncnt[threadIdx.x] > k.nz_cap) {   // ncnt holds the node totals here
     double a = 0.0;
     for (int w = 0; w < NW; w++) a += s.spart[w * kBC + threadIdx.x];
     k.sums2[(int64_t)g * kBC + threadIdx.x] = a;
@@ -505,6 +655,9 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     s.wready = s.sready + 2;
     s.flags = reinterpret_cast<int*>(s.wready + 2);
     s.rel = reinterpret_cast<unsigned*>(s.flags + kBC);
+    s.ncnt = reinterpret_cast<int*>(s.rel + NST);
+    s.stile = s.ncnt + kBC;
+    s.sched = s.stile + NST;
   }
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -522,7 +675,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   }
   __syncthreads();
   unsigned phases = 0, hph = 0;
-  if (tid == 0) prefill(k, s);
+  if (tid == 0) prefill(k, s, 0);
 
   // u0 = Z (c + ρβ0 − v0), then the warm/cold refresh sweep (R6)
   sweep<SW_FWD_W, KS, MT>(k, s, false, false, phases, hph);
@@ -541,15 +694,30 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     PROF_ACC(6);
     grid_sync(k.bar);
     reduce_u(k, s, k.U);
+    __shared__ int tot_s[kBC];
+    if (chk) compact_nonzeros(k, tot_s);   // β⁺'s nonzeros → dense per-node lists
     grid_sync(k.bar);
     PROF_ACC(7);
     if (!chk) continue;
-    sweep<SW_FWD_BETA, KS, MT>(k, s, false, false, phases, hph);
+    PROF_RESET();
+    // primal ‖Xβ‖²: a gather over β⁺'s nonzeros (sparse at the paper's workloads); a node with
+    // more than nz_cap nonzeros falls back to one forward-only sweep Zβ and ‖L(Zβ)‖²
+    {
+      gather_partial(k, s, tot_s);
+      bool dense = false;
+      if (tid < kBC) s.ncnt[tid] = tot_s[tid];
+      __syncthreads();
+      for (int nd = 0; nd < kBC; nd++) dense |= (s.flags[nd] & F_ACTIVE) && tot_s[nd] > k.nz_cap;
+      if (dense) {
+        sweep<SW_FWD_BETA, KS, MT>(k, s, false, false, phases, hph);
+        grid_sync(k.bar);
+        reduce_u(k, s, k.Ub);
+        grid_sync(k.bar);
+        lmatvec_partial(k, s);
+      }
+    }
     grid_sync(k.bar);
-    reduce_u(k, s, k.Ub);
-    grid_sync(k.bar);
-    lmatvec_partial(k, s);
-    grid_sync(k.bar);
+    PROF_ACC(5);
     // every CTA derives the same per-node decision from the same partials (fixed order)
     if (tid < kBC) {
       const int nd = tid;
@@ -584,11 +752,8 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     if (!any) break;
   }
   // drain the prefill issued after the last sweep before the CTA retires
-  if (tid == 0) {
-    const int g = blockIdx.x, G = gridDim.x;
-    const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
-    for (int sg = 0; sg < NST && t0 + sg < t1; sg++) mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
-  }
+  if (tid == 0)
+    for (int sg = 0; sg < NST && sg < s.sched[1]; sg++) mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
   if (blockIdx.x == 0 && tid < k.nb) {
     const int nd = tid;
     const double lbb = s.red[nd], plb = __ldcg(k.nodef + nd * 4 + 2);
@@ -773,7 +938,7 @@ int debug_prof(unsigned long long*, int) { return 0; }
 
 size_t admm_smem_bytes(int64_t ld) {
   return sizeof(double) * ((size_t)NST * kPt * ld + NST * STQ + 2 * NMW * 64 + 2 * kBC * 12 + 64 * 4 + kBC) +
-         (NST + 4) * sizeof(uint64_t) + kBC * sizeof(int) + NST * sizeof(unsigned) + 64;
+         (NST + 4) * sizeof(uint64_t) + 2 * kBC * sizeof(int) + (NST + 4) * sizeof(int) + NST * sizeof(unsigned) + 64;
 }
 
 int admm_alloc(Ctx* c) {
@@ -794,6 +959,17 @@ int admm_alloc(Ctx* c) {
   c->Upart = (double*)dalloc(c, sizeof(double) * c->grid * kBC * ld);
   c->sums = (double*)dalloc(c, sizeof(double) * c->grid * kBC * kSums);
   c->sums2 = (double*)dalloc(c, sizeof(double) * c->grid * kBC);
+  // sparse primal check: per-CTA segments of β⁺'s nonzeros (capacity = the CTA's columns) and the
+  // dense per-node lists (capacity p/16: above it the forward-only Zβ sweep is cheaper)
+  c->seg_cap = (int)((ntiles + c->grid - 1) / c->grid) * (kPt / NEW);   // columns per (CTA, epilogue warp)
+  c->nz_cap = (int)std::max<int64_t>(256, round8(c->p) / 16);
+  c->seg_idx = (int32_t*)dalloc(c, sizeof(int32_t) * c->grid * NEW * kBC * c->seg_cap);
+  c->seg_val = (double*)dalloc(c, sizeof(double) * c->grid * NEW * kBC * c->seg_cap);
+  c->seg_cnt = (int*)dalloc(c, sizeof(int) * c->grid * NEW * kBC);
+  c->nz_idx = (int32_t*)dalloc(c, sizeof(int32_t) * kBC * c->nz_cap);
+  c->nz_val = (double*)dalloc(c, sizeof(double) * kBC * c->nz_cap);
+  if (!c->seg_idx || !c->seg_val || !c->seg_cnt || !c->nz_idx || !c->nz_val)
+    return set_err(c, L0L2_ENOMEM, "sparse check work space");
   c->node_f = (double*)dalloc(c, sizeof(double) * kBC * 4);
   c->node_i = (int*)dalloc(c, sizeof(int) * kBC * 2);
   c->bar = (unsigned*)dalloc(c, sizeof(unsigned) * 2);
@@ -842,8 +1018,15 @@ int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st) {
   k.beta = c->beta; k.v = c->v; k.bchk = c->bchk; k.code = c->code;
   k.U = c->U; k.Ub = c->Ub; k.Upart = c->Upart; k.sums = c->sums; k.sums2 = c->sums2;
   k.nodef = c->node_f; k.nodei = c->node_i; k.bar = c->bar;
+  k.seg_idx = c->seg_idx; k.seg_val = c->seg_val; k.seg_cnt = c->seg_cnt; k.nz_idx = c->nz_idx; k.nz_val = c->nz_val;
+  k.X = c->X; k.seg_cap = c->seg_cap; k.nz_cap = c->nz_cap;
+  if (const char* e = getenv("L0L2_NZCAP")) k.nz_cap = std::min(k.nz_cap, atoi(e));   // testing hook (0 = always sweep)
   k.out_lb = a.lb; k.out_primal = a.primal; k.out_iters = a.iters; k.out_flags = a.flags;
   k.ld = c->ld; k.n = c->n; k.n8 = round8(c->n); k.p8 = round8(c->p);
+  k.pfd = PFD_DEFAULT;
+  k.pfs = 0;
+  if (const char* e = getenv("L0L2_PFS")) k.pfs = std::max(0, atoi(e));   // tuning hook
+  if (const char* e = getenv("L0L2_PFD")) k.pfd = std::max(0, atoi(e));   // tuning hook
   k.ntiles = (int)(k.p8 / kPt); k.nb = a.nb; k.check_every = c->check_every; k.max_iters = c->max_iters;
   k.rho = c->rho; k.inv_rho = 1.0 / c->rho; k.lam0 = c->lam0; k.lam2 = c->lam2; k.M = c->M; k.yy = c->yy;
   k.node_tol = c->node_tol;

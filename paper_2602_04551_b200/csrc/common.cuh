@@ -45,7 +45,12 @@ struct Ctx {
   double *U = nullptr, *Ub = nullptr;                       // [kBC][ld]
   double *Upart = nullptr;                                  // [grid][kBC][ld]
   double *sums = nullptr;                                   // [grid][kBC][kSums]
-  double *sums2 = nullptr;                                  // [grid][kBC] ‖L Zβ‖² partials
+  double *sums2 = nullptr;                                  // [grid][kBC] ‖Xβ‖² partials
+  int32_t *seg_idx = nullptr, *nz_idx = nullptr;            // sparse primal check (admm.cu)
+  double *seg_val = nullptr, *nz_val = nullptr;
+  int *seg_cnt = nullptr;
+  int seg_cap = 0, nz_cap = 0;
+
   double *node_f = nullptr;                                 // per-node scalars (admm.cu)
   int *node_i = nullptr;
   int *badflag = nullptr;

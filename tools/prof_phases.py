@@ -33,7 +33,7 @@ epi = a[:, 14:16, :].mean(axis=(0, 1))
 w0 = a[:, 0, :].mean(axis=0)
 print("MMA warps  (cycles/warp): stage-wait %.3g adj %.3g wready-wait %.3g fwd %.3g release %.3g" % tuple(mma[:5]))
 print("epi warps  (cycles/warp): stage-wait %.3g pre %.3g sready-wait %.3g partials %.3g xwait %.3g math %.3g" % tuple(epi[:6]))
-print("warp 0 loop: fused sweeps %.3g, sync+reduce %.3g" % (w0[6], w0[7]))
+print("warp 0 loop: fused sweeps %.3g, sync+reduce %.3g, check phase %.3g" % (w0[6], w0[7], w0[5]))
 s6 = a[:, 0, 6]
 s7 = a[:, 0, 7]
 print("per-CTA fused sweeps: min %.4g mean %.4g max %.4g; sync+reduce min %.4g mean %.4g max %.4g"
