@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-certified", action="store_true")
+    ap.add_argument("--no-microbench", action="store_true")
+    ap.add_argument("--micro-iters", type=int, default=100)
     ap.add_argument("--verbose", action="store_true")
     return ap.parse_args()
 
@@ -128,6 +130,59 @@ class ClockSampler:
         reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
+
+
+FP64_DMMA_PEAK_TFLOPS = 37.1   # measured: tools/microbench/fp64_peaks.cu on this pool's B200 (profiles/)
+
+
+def roofline_of(flops, nbytes, seconds, hbm_peak):
+    """achieved ÷ min(FP64 peak, AI·BW peak), AI = algorithmic flops / bytes."""
+    ai = flops / nbytes
+    ridge_tf = ai * hbm_peak / 1e3
+    tf = flops / seconds / 1e12
+    gbs = nbytes / seconds / 1e9
+    if ridge_tf < FP64_DMMA_PEAK_TFLOPS:
+        return dict(bound="hbm", achieved=gbs, peak=hbm_peak, unit="GB/s", frac=gbs / hbm_peak, ai=ai,
+                    fp64_tflops=tf)
+    return dict(bound="tensor", achieved=tf, peak=FP64_DMMA_PEAK_TFLOPS, unit="TFLOP/s",
+                frac=tf / FP64_DMMA_PEAK_TFLOPS, ai=ai, achieved_gbs=gbs)
+
+
+def bound_microbench(inst, rho, device, iters, Bs=(1, 2, 4, 8, 16, 32, 64, 128)):
+    """SURVEY §8(d) microbenchmark, independent of tree width: l0l2_bound_batch on node sets with
+    random fixings at depth 5-10 and parent-warm states from a prior call, a fixed `iters`
+    iterations (node_tol disabled), X resident.  Per B: node-iterations/s of the whole call and the
+    ADMM kernel's roofline fraction from its CUDA-event time."""
+    import torch
+    import synth
+    from paper_2602_04551_b200 import Problem
+    peak, _ = measured_peaks()
+    pr = Problem(np.asfortranarray(inst.X), inst.y, inst.lambda0, inst.lambda2, inst.M, rho=rho, node_tol=-1.0,
+                 max_iters=iters, device=device)
+    B_max = max(Bs)
+    fx = [((), ())] + synth.random_fixings(inst.p, B_max - 1, seed=11, depth_lo=5, depth_hi=10,
+                                           prefer=inst.support_true)
+    warm = pr.l0l2_bound_batch(fx)["warm_out"]
+    rows = []
+    for B in Bs:
+        pr.l0l2_bound_batch(fx[:B], warm_in=warm[:B])   # warm-up
+        torch.cuda.synchronize(device)
+        pr.l0l2_kernel_stats(reset=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pr.l0l2_bound_batch(fx[:B], warm_in=warm[:B])
+        e1.record()
+        torch.cuda.synchronize(device)
+        ms = e0.elapsed_time(e1)
+        ks = pr.l0l2_kernel_stats()
+        r = roofline_of(ks["admm_flops_alg"], ks["admm_bytes_alg"], ks["admm_ms"] / 1e3, peak)
+        rows.append({"B": B, "call_ms": ms, "node_iters_per_s": B * (iters + 1) / (ms / 1e3),
+                     "admm_ms": ks["admm_ms"], "launches": ks["admm_launches"],
+                     "ms_per_iteration_per_launch": ks["admm_ms"] / ks["admm_launches"] / (iters + 1),
+                     "roofline": r})
+    pr.close()
+    return {"workload": "l0l2_bound_batch, %d fixed iterations, random fixings depth 5-10, parent-warm" % iters,
+            "rows": rows}
 
 
 def oracle_iters_per_node(cfg):
@@ -287,15 +342,21 @@ def main():
     achieved = ks["admm_bytes_alg"] / (ks["admm_ms"] / 1e3) / 1e9 if ks["admm_ms"] > 0 else 0.0
     per_launch_bytes = ks["admm_bytes_alg"] / max(1, ks["admm_launches"])
     tr = ncu_traffic()
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": (tr * per_launch_bytes) if tr else None,
-            "kernel": "admm_persistent", "peak_source": peak_src,
-            "launches": ks["admm_launches"], "avg_launch_ms": ks["admm_ms"] / max(1, ks["admm_launches"]),
-            "alg_bytes_per_launch": per_launch_bytes,
-            "fp64_tflops": ks["admm_flops_alg"] / (ks["admm_ms"] / 1e3) / 1e12 if ks["admm_ms"] > 0 else 0.0,
-            "share_of_step": ks["admm_ms"] / max(1e-9, ms / world if world > 1 else ms)}
+    roof = roofline_of(ks["admm_flops_alg"], ks["admm_bytes_alg"], ks["admm_ms"] / 1e3, peak)
+    roof.update({"traffic": (tr * per_launch_bytes) if tr else None,
+                 "kernel": "admm_persistent",
+                 "peak_source": (peak_src if roof["bound"] == "hbm" else
+                                 "measured FP64 DMMA peak (tools/microbench/fp64_peaks.cu, profiles/)"),
+                 "hbm_gbs": achieved, "hbm_frac": achieved / peak,
+                 "launches": ks["admm_launches"], "avg_launch_ms": ks["admm_ms"] / max(1, ks["admm_launches"]),
+                 "alg_bytes_per_launch": per_launch_bytes,
+                 "alg_flops_per_launch": ks["admm_flops_alg"] / max(1, ks["admm_launches"]),
+                 "share_of_step": ks["admm_ms"] / max(1e-9, ms / world if world > 1 else ms)})
     prob.close()
     del prob
+    micro = None
+    if world == 1 and not args.no_microbench:
+        micro = bound_microbench(inst, rho, local, args.micro_iters)
 
     # ------------------------------------------------------------------ end-to-end arm (host buffers)
     import torch as _t
@@ -368,6 +429,8 @@ def main():
                 "roofline": roof, "e2e": e2e, "clocks": clk.summary()}
         if certified is not None:
             line["certified_solves"] = certified
+        if micro is not None:
+            line["bound_microbench"] = micro
         if cpu is not None:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(line), flush=True)

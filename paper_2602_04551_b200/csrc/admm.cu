@@ -1,5 +1,5 @@
 // Batched ADMM node lower bound (§3.1-§3.2) as ONE persistent,
-// cooperative sm_100a kernel per group of kBC = 8 nodes.
+// cooperative sm_100a kernel per group of kBC = 16 nodes.
 //
 // Per iteration t and node k (state β, v in HBM, layout [p][kBC] node-minor):
 //   w  = c + ρβ − v                              (eq:b_update)
@@ -11,17 +11,26 @@
 //
 // One-pass mapping: because the prox, the v-update and the next w
 // are elementwise in the coordinate j, one sweep over 8-column tiles Z_J of Z does
-//   adjoint  S_J = Z_Jᵀ u          (DMMA m8n8k4, K = n split over 16 warps)
+//   adjoint  S_J = Z_Jᵀ u          (DMMA m8n8k4, K = n split over 14 warps)
 //   epilogue b, β⁺, v⁺, w⁺ and the check sums for the 8×8 (column, node) block
 //   forward  u⁺ += Z_J w⁺_J        (DMMA, accumulators in registers)
-// from the SAME shared-memory copy of Z_J (a cp.async.bulk / TMA bulk copy, double buffered
-// with an mbarrier), so Z is read from HBM once per iteration.  The per-CTA forward partials
-// are then reduced across the grid in a fixed order (deterministic, independent of B).
+// from the SAME shared-memory copy of Z_J (a cp.async.bulk / TMA bulk copy, 3-stage ring
+// with mbarriers), so Z is read from HBM once per iteration.
+//
+// Node halves and CTA pairs.  A CTA holds u (n×8) and its forward accumulator (n×8) in
+// registers — half the register file each — so one CTA serves one node half (8 nodes).  Z's
+// tiles are cut into G = grid fixed sub-ranges.  When both halves of the group have active
+// nodes, CTAs 2P and 2P+1 both stream sub-ranges 2P and 2P+1 in the same order, one per half:
+// the second read of each tile is an L2 hit, so HBM sees Z once per iteration for 16 nodes and
+// every SM does 8-node DMMA work on twice the tiles (FP64-bound instead of HBM-bound).  When
+// only one half is active, every CTA streams its own sub-range for that half.  Forward partials,
+// check sums and nonzero lists are kept per sub-range and reduced across the grid in a fixed
+// order, so a node's arithmetic is bitwise the same in either mode, in any slot, for any B.
 //
 // Checks (every check_every iterations) use identities that need no pass over X:
 //   Xᵀr̂ = c − s,  ‖X b‖² = bᵀs   ⇒  dual(r̂ = y − Xb) = ½‖y‖² − ½ bᵀs − Σ ν_j(|c_j − s_j|)
-//   primal P(β) = ½‖y‖² − cᵀβ + ½‖L(Zβ)‖² + Σ ψ_j(β_j)
-// where Zβ is one extra forward-only sweep on check iterations.
+//   primal P(β) = ½‖y‖² − cᵀβ + ½‖Xβ‖² + Σ ψ_j(β_j)
+// where ‖Xβ‖² is a gather over β⁺'s nonzeros (dense β⁺: one forward-only sweep Zβ, ‖L(Zβ)‖²).
 #include <cmath>
 #include <cstdlib>
 
@@ -32,6 +41,8 @@ namespace {
 
 constexpr int NW = kAdmmThreads / 32;   // 16 warps: 14 MMA + 2 epilogue
 constexpr int NEW = 2;                  // epilogue warps
+constexpr int NH = kBC / 8;             // node halves (one per CTA of a pair)
+static_assert(NH == 2, "a CTA pair serves the two node halves");
 constexpr int F_ACTIVE = 8;             // internal node flag bit (not exported)
 
 struct KP {
@@ -52,8 +63,9 @@ struct KP {
   unsigned* bar;                   // [2]: count, generation
   double* out_lb; double* out_primal; int* out_iters; uint8_t* out_flags;
   int64_t ld, n, n8, p8;
-  int ntiles, nb, check_every, max_iters, pfd;
+  int ntiles, nsr, nb, check_every, max_iters, pfd;   // nsr: tile sub-ranges (= grid)
   int pfs;                         // tiles L2-prefetched by prefill (during the grid reduction)
+  int tsplit;                      // bulk copies per Z tile (divides kPt)
   double rho, inv_rho, lam0, lam2, M, yy, node_tol;
   double shrink, sr, a_l1, a_4, psi_l1, psi_4, zsr;
   bool sr_le_M;
@@ -168,21 +180,26 @@ constexpr int PFD_DEFAULT = 1; // additional tiles prefetched into L2 beyond the
 constexpr int NMW = NW - 2;    // MMA warps (adjoint + forward); the last 2 warps run the epilogue
 constexpr int MMA_THREADS = NMW * 32;
 // n classes of the kernel: KS adjoint k-steps (4 rows) and MT forward row tiles (8 rows) per MMA
-// warp, so n8 ≤ min(4·NMW·KS, 8·NMW·MT).  (19, 10) is the largest: n ≤ 1064.
+// warp, so n8 ≤ min(4·NMW·KS, 8·NMW·MT).  (19, 10) is the largest: n ≤ 1064.  (16 MMA warps would
+// balance the 4 SM sub-partitions, but 18 warps leave 96 registers per thread: u and the forward
+// accumulators no longer fit.)
 constexpr int NCLS = 5;
 constexpr int CLS_KS[NCLS] = {2, 5, 10, 18, 19};
 constexpr int CLS_MT[NCLS] = {1, 3, 5, 9, 10};
 
 // Per-stage copy of the epilogue's operands for tile J, TMA'd with Z_J on the same mbarrier:
-//   β_J [8][8], v_J [8][8], c_J [8], code_J [8][8] bytes (node-minor, as in HBM)
-constexpr int STQ = 64 + 64 + 8 + 8;                       // doubles per stage
-constexpr unsigned STQ_BYTES = 512 + 512 + 64 + 64;
+//   β_J [8][kBC], v_J [8][kBC], c_J [8], code_J [8][kBC] bytes (node-minor, as in HBM; a CTA
+//   uses its half's 8 nodes of each row)
+constexpr int STB = kPt * kBC;                             // (column, node) elements per tile
+constexpr int STQ = STB + STB + 8 + STB / 8;               // doubles per stage
+constexpr unsigned STQ_BYTES = 8 * STB + 8 * STB + 64 + STB;
 
 struct Smem {
   double* tiles;      // [NST][kPt][ld]   Z_J ring (stage q at tiles + q·kPt·ld)
   double* stq;        // [NST][STQ]       β_J, v_J, c_J, code_J of the staged tile
   double* spart;      // [2][NMW][64]     adjoint partials per MMA warp (double buffered)
-  double* Ws;         // [2][kBC][12]     w⁺_J (node-major, padded; double buffered)
+  double* Ws;         // [2][8][12]       w⁺_J of the CTA's half (node-major, padded; double
+                      //                  buffered), then [2 sub-ranges][64][4] check-sum stash
   double* red;        // [kBC]            running max of checked duals (R7)
   uint64_t* mbar;     // [NST]
   uint64_t* sready;   // [2]              S_J partials ready / w⁺ buffer free (NMW arrivals)
@@ -191,7 +208,9 @@ struct Smem {
   unsigned* rel;      // [NST] MMA warps done with the stage (last one refills it)
   int* ncnt;          // [kBC]            per-node β⁺ nonzero totals at a check (lmatvec fallback)
   int* stile;         // [NST]            tile held by each ring slot (−1: end of this CTA's sweep)
-  int* sched;         // [4]              sweep number, stages issued, tiles taken, done (issuer only)
+  int* sched;         // [9]              sweep number, stages issued, tiles taken, done (issuer
+                      //                  only); node half, paired, tile range [t0, t1) of the sweep,
+                      //                  issue deferred
 };
 
 // Producer → consumer hand-offs inside the CTA are mbarriers, not named barriers: a named barrier
@@ -225,26 +244,31 @@ __device__ __forceinline__ unsigned tile_bytes(const KP& k) { return (unsigned)(
 __device__ __forceinline__ void issue_stage(const KP& k, Smem& s, int t, int sg) {
   const unsigned tb = tile_bytes(k);
   mbar_expect_tx(&s.mbar[sg], tb + STQ_BYTES);
-  bulk_g2s(s.tiles + (size_t)sg * kPt * k.ld, k.Z + (int64_t)t * kPt * k.ld, tb, &s.mbar[sg]);
+  // Z_J as k.tsplit bulk copies of kPt/tsplit whole columns each (more requests in flight)
+  const int cpc = kPt / k.tsplit;
+  for (int c = 0; c < kPt; c += cpc)
+    bulk_g2s(s.tiles + (size_t)sg * kPt * k.ld + c * k.ld, k.Z + ((int64_t)t * kPt + c) * k.ld,
+             (unsigned)(cpc * k.ld * sizeof(double)), &s.mbar[sg]);
   double* q = s.stq + sg * STQ;
-  bulk_g2s(q, k.beta + (int64_t)t * kPt * kBC, 512, &s.mbar[sg]);
-  bulk_g2s(q + 64, k.v + (int64_t)t * kPt * kBC, 512, &s.mbar[sg]);
-  bulk_g2s(q + 128, k.c + (int64_t)t * kPt, 64, &s.mbar[sg]);
-  bulk_g2s(q + 136, k.code + (int64_t)t * kPt * kBC, 64, &s.mbar[sg]);
+  bulk_g2s(q, k.beta + (int64_t)t * STB, 8 * STB, &s.mbar[sg]);
+  bulk_g2s(q + STB, k.v + (int64_t)t * STB, 8 * STB, &s.mbar[sg]);
+  bulk_g2s(q + 2 * STB, k.c + (int64_t)t * kPt, 64, &s.mbar[sg]);
+  bulk_g2s(q + 2 * STB + 8, k.code + (int64_t)t * STB, STB, &s.mbar[sg]);
 }
 
-// Tile scheduling.  Every sweep streams all tiles of Z once; CTA g owns the fixed contiguous
-// range [t0, t1) (bitwise deterministic, independent of the batch composition).  The stages a
-// CTA consumes are numbered m = 0, 1, ... in ring order (slot m % NST); one thread issues each
-// (issue_next).  After the CTA's last tile one end-marker stage (tile −1, a plain arrive, no
-// copy) is issued and consumers stop at it.  The tile id is written before the (release) arrive,
-// so every consumer reads it after its (acquire) wait on the stage's mbarrier.  (A dynamic,
-// grid-wide ticket schedule was measured and gave nothing: the sweep is bound by aggregate HBM
-// bandwidth, not by the slowest SM — DESIGN.md §4.)
+// Tile scheduling.  Every sweep streams all tiles of Z once.  Sub-range r < G = gridDim.x is
+// the fixed tile range [T(r), T(r+1)), T(r) = ⌊ntiles·r/G⌋ (bitwise deterministic, independent of
+// the batch composition).  The CTA streams one contiguous range per sweep (set by prefill: its own
+// sub-range, or its pair's two).  The stages a CTA consumes are numbered m = 0, 1, ... in ring
+// order (slot m % NST); one thread issues each (issue_next).  After the CTA's last tile one
+// end-marker stage (tile −1, a plain arrive, no copy) is issued and consumers stop at it.  The tile
+// id is written before the (release) arrive, so every consumer reads it after its (acquire) wait on
+// the stage's mbarrier.  (A dynamic, grid-wide ticket schedule was measured and gave nothing.)
+__device__ __forceinline__ int sub_t(const KP& k, int r) { return (int)((int64_t)k.ntiles * r / k.nsr); }
+
 __device__ void issue_next(const KP& k, Smem& s) {
   if (s.sched[3]) return;
-  const int g = blockIdx.x, G = gridDim.x;
-  const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
+  const int t0 = s.sched[6], t1 = s.sched[7];
   const int sg = s.sched[1] % NST;
   const int tile = t0 + s.sched[2] < t1 ? t0 + s.sched[2] : -1;
   s.stile[sg] = tile;
@@ -260,20 +284,43 @@ __device__ void issue_next(const KP& k, Smem& s) {
   }
 }
 
-// Start sweep number `sw`: issue its first NST stages.  Called by thread 0 once before the first
-// sweep and again at the end of every sweep, so the next sweep's first tiles stream in while the
-// grid reduces u.  The β, v of any tile were written by some CTA's epilogue threads in an earlier
-// sweep (generic → async proxy fence, then grid barrier) before a stage can read them.
+// Start sweep number `sw`: choose the CTA's node half and tile range from the node flags, then
+// issue the first NST stages.  Called by thread 0 once before the first sweep and again at the end
+// of every sweep (so the next sweep's first tiles stream in while the grid reduces u; the flags it
+// sees may still include nodes that the coming check retires, which only costs idle DMMA slots).
+// Paired: both halves active → CTA g serves half g&1 on sub-ranges 2⌊g/2⌋, 2⌊g/2⌋+1.  Otherwise
+// CTA g serves the active half on sub-range g.  Every CTA decides from the same flags.  While the
+// mode stays, the CTA's next tiles hold β, v rows of its half that it wrote itself (epilogue
+// threads: generic → async proxy fence, then the CTA barrier before this call).  When the mode
+// changes, those rows may have been written by the partner CTA, which may still be sweeping: the
+// issue is deferred (sched[8]) to the start of the next sweep, which follows a grid barrier.
+__device__ void issue_first(const KP& k, Smem& s) {
+  for (int m = 0; m < NST; m++) issue_next(k, s);
+  // the grid reduction that follows leaves HBM idle: pull the sweep's next tiles into L2 meanwhile
+  const int t0 = s.sched[6], t1 = s.sched[7];
+  for (int t = t0 + NST + k.pfd; t < t1 && t < t0 + NST + k.pfs; t++) prefetch_l2(k.Z + (int64_t)t * kPt * k.ld, tile_bytes(k));
+}
+
 __device__ void prefill(const KP& k, Smem& s, int sw) {
+  const int g = blockIdx.x;
+  int a0 = 0, a1 = 0;
+  for (int nd = 0; nd < 8; nd++) {
+    a0 |= s.flags[nd] & F_ACTIVE;
+    a1 |= s.flags[8 + nd] & F_ACTIVE;
+  }
+  const bool paired = a0 && a1;
+  const int half = paired ? (g & 1) : (a0 ? 0 : 1);
+  const bool changed = sw > 0 && (half != s.sched[4] || (int)paired != s.sched[5]);
+  s.sched[4] = half;
+  s.sched[5] = paired;
+  s.sched[6] = paired ? sub_t(k, g & ~1) : sub_t(k, g);
+  s.sched[7] = paired ? sub_t(k, (g & ~1) + 2) : sub_t(k, g + 1);
   s.sched[0] = sw;
   s.sched[1] = 0;
   s.sched[2] = 0;
   s.sched[3] = 0;
-  for (int m = 0; m < NST; m++) issue_next(k, s);
-  // the grid reduction that follows leaves HBM idle: pull the sweep's next tiles into L2 meanwhile
-  const int g = blockIdx.x, G = gridDim.x;
-  const int t0 = (int)((int64_t)k.ntiles * g / G), t1 = (int)((int64_t)k.ntiles * (g + 1) / G);
-  for (int t = t0 + NST + k.pfd; t < t1 && t < t0 + NST + k.pfs; t++) prefetch_l2(k.Z + (int64_t)t * kPt * k.ld, tile_bytes(k));
+  s.sched[8] = changed;
+  if (!changed) issue_first(k, s);
 }
 
 // One sweep over this CTA's tiles, warp-specialised:
@@ -281,14 +328,25 @@ __device__ void prefill(const KP& k, Smem& s, int sw) {
 //   epilogue warps:        for t: wait S(t) → b, β⁺, v⁺, w⁺, check sums → publish w⁺(t)
 // so the elementwise epilogue of tile t overlaps the DMMA adjoint of tile t+1.  u of this
 // iteration lives in registers as the adjoint's B fragments (MMA warp w owns k-steps [ks0, ks1),
-// lane holds U[row = 4q + lane%4][node = lane/4]).  Forward partials go to Upart[cta], check sums
-// to sums[cta].
+// lane holds U[row = 4q + lane%4][node = 8h + lane/4]).  Forward partials go to Upart[sub-range],
+// check sums to sums[sub-range], per sub-range (a paired CTA flushes at its sub-range boundary).
 template <int MODE, int KS, int MT>
 __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& phases, unsigned& hph) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.x;
   constexpr bool fused = (MODE == SW_FUSED);
   const bool is_mma = warp < NMW;
+  // this sweep's node half and sub-ranges (fixed by prefill; s.sched[4..7] do not change until
+  // the CTA barrier at the end of the sweep)
+  const int h = s.sched[4];
+  const bool paired = s.sched[5] != 0;
+  const int sr0 = paired ? (g & ~1) : g;
+  const int tb = paired ? sub_t(k, sr0 + 1) : 0x7fffffff;   // first tile of the second sub-range
+  if (s.sched[8]) {   // deferred by a mode change (prefill); a grid barrier has passed.  (sched[8]
+                      // is rewritten only by the next prefill, so every thread takes this branch.)
+    if (tid == 0) issue_first(k, s);
+    __syncthreads();   // orders the scheduler state before the in-sweep issuers (acq_rel below)
+  }
   // wait for ring stage m; returns its tile (−1: the CTA's sweep is over)
   auto stage = [&](int m) {
     const int sg = m % NST;
@@ -310,15 +368,34 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
 #pragma unroll
     for (int i = 0; i < MT; i++) acc[i][0] = acc[i][1] = 0.0;
     double uf[KS];
+    const bool uact = (s.flags[8 * h + cA] & F_ACTIVE) != 0;
 #pragma unroll
     for (int i = 0; i < KS; i++) {
       const int q = warp + NMW * i;
-      uf[i] = (fused && q < kt) ? __ldcg(k.U + cA * ld + q * 4 + kA) : 0.0;
+      uf[i] = (fused && uact && q < kt) ? __ldcg(k.U + (8 * h + cA) * ld + q * 4 + kA) : 0.0;
     }
+    // this CTA's forward partial of sub-range sr: Upart[sr][8h + node][row]; then restart
+    auto flush = [&](int sr) {
+      double* up = k.Upart + ((int64_t)sr * kBC + 8 * h) * k.ld;
+#pragma unroll
+      for (int i = 0; i < MT; i++) {
+        const int m = warp + i * NMW;
+        if (m < mt) {
+          const int row = m * 8 + (lane >> 2), nd = 2 * (lane & 3);
+          up[(int64_t)nd * k.ld + row] = acc[i][0];
+          up[(int64_t)(nd + 1) * k.ld + row] = acc[i][1];
+        }
+        acc[i][0] = acc[i][1] = 0.0;
+      }
+    };
+    bool flushed = !paired;
+    int ctile = -1;   // tile of stage m (forward)
     // adjoint of stage m (fused sweeps); false at the end marker
+    int ntile = -1;
     auto adjoint = [&](int m) {
       PROF_T0();
       const int tile = stage(m);
+      ntile = tile;
       PROF_ACC(0);
       if (tile < 0) return false;
       const double* T = s.tiles + (size_t)(m % NST) * kPt * ld + cA * ld + kA;
@@ -333,16 +410,19 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       PROF_ACC(1);
       return true;
     };
-    bool cur = fused ? adjoint(0) : stage(0) >= 0;
+    bool cur;
+    if (fused) { cur = adjoint(0); ctile = ntile; }
+    else { ctile = stage(0); cur = ctile >= 0; }
     for (int m = 0; cur; m++) {
       const int sg = m % NST;
       const bool nxt = fused ? adjoint(m + 1) : true;
       PROF_T0();
+      if (!flushed && ctile >= tb) { flush(sr0); flushed = true; }
       mbar_wait(&s.wready[m & 1], (hph >> (m & 1)) & 1u);   // w⁺_J(m) published
       hph ^= 1u << (m & 1);
       PROF_ACC(2);
       const double* T = s.tiles + (size_t)sg * kPt * ld + kA * ld + cA;
-      const double* W = s.Ws + (m & 1) * kBC * 12;
+      const double* W = s.Ws + (m & 1) * 8 * 12;
       // ---- forward: U⁺(rows × 8 nodes) += Z_J (rows × 8 cols) · W_J (8 cols × 8 nodes)
       const double b0 = W[cA * 12 + kA];         // B[k = j][n = node]
       const double b1 = W[cA * 12 + 4 + kA];
@@ -355,10 +435,10 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       PROF_ACC(3);
       if (!fused) mbar_arrive_warp(&s.sready[m & 1]);   // w⁺ buffer m&1 free again
       // release stage m: the last MMA warp to finish its forward refills the slot (no CTA barrier;
-      // acq_rel orders the scheduler state between successive issuing lanes)
+      // acq_rel orders the scheduler state (s.sched) between successive issuing lanes).  (Issuing
+      // from an epilogue warp instead was measured slower: the refill then waits for the epilogue.)
       __syncwarp();
       if (lane == 0) {
-        // acq_rel: orders the scheduler state (s.sched) between successive issuing lanes
         unsigned old;
         asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(saddr(&s.rel[sg])) : "memory");
         if (old == NMW - 1) {
@@ -368,38 +448,44 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       }
       __syncwarp();
       PROF_ACC(4);
-      cur = fused ? nxt : stage(m + 1) >= 0;
+      if (fused) { cur = nxt; ctile = ntile; }
+      else { ctile = stage(m + 1); cur = ctile >= 0; }
     }
-    // ---- this CTA's forward partial: Upart[g][node][row]
-    double* up = k.Upart + (int64_t)g * kBC * k.ld;
-#pragma unroll
-    for (int i = 0; i < MT; i++) {
-      const int m = warp + i * NMW;
-      if (m < mt) {
-        const int row = m * 8 + (lane >> 2), nd = 2 * (lane & 3);
-        up[(int64_t)nd * k.ld + row] = acc[i][0];
-        up[(int64_t)(nd + 1) * k.ld + row] = acc[i][1];
-      }
-    }
+    if (!flushed) flush(sr0);
+    flush(paired ? sr0 + 1 : sr0);
   } else {
-    // ---------------- epilogue warps: element (j = et>>3, node = et&7) of each 8×8 block
-    const int et = tid - MMA_THREADS, j = et >> 3, nd = et & 7;
-    const bool active = (s.flags[nd] & F_ACTIVE) != 0;
+    // ---------------- epilogue warps: element (j = et>>3, node = 8h + (et&7)) of each 8×8 block
+    const int et = tid - MMA_THREADS, j = et >> 3, nd = et & 7, node = 8 * h + nd;
+    const bool active = (s.flags[node] & F_ACTIVE) != 0;
     double sT1 = 0.0, sT2 = 0.0, sT3 = 0.0, sT4 = 0.0;
     const int ew = et >> 5;   // epilogue warp: columns 4·ew .. 4·ew + 3 of each tile
-    int seg_n = 0;            // β⁺ nonzeros of (this CTA, warp ew, node nd) so far (check sweeps)
+    int seg_n = 0;            // β⁺ nonzeros of (sub-range, warp ew, node) so far (check sweeps)
+    int sr = sr0;             // sub-range of the current tile
+    // close sub-range sr: its nonzero count and its check sums (stash slot sr − sr0)
+    auto eflush = [&]() {
+      if (fused && check) {
+        if ((et & 31) < 8) k.seg_cnt[((int64_t)sr * NEW + ew) * kBC + node] = seg_n;
+        double* st = s.Ws + 2 * 8 * 12 + ((sr - sr0) * 64 + et) * 4;
+        st[0] = sT1; st[1] = sT2; st[2] = sT3; st[3] = sT4;
+      }
+      sT1 = sT2 = sT3 = sT4 = 0.0;
+      seg_n = 0;
+      sr++;
+    };
     int m = 0;
     for (;; m++) {
       PROF_T0();
       const int tile = stage(m);   // stage m landed (its state operands too), or the end marker
       PROF_ACC(0);
       if (tile < 0) break;
+      if (paired && sr == sr0 && tile >= tb) eflush();
       const int sg = m % NST;
       const int64_t col0 = (int64_t)tile * kPt;
-      const int64_t e = (col0 + j) * kBC + nd;
+      const int el = j * kBC + node;
+      const int64_t e = col0 * kBC + el;
       const double* q = s.stq + sg * STQ;
-      const double st_beta = q[et], st_v = q[64 + et], st_c = q[128 + j];
-      const uint8_t st_code = reinterpret_cast<const uint8_t*>(q + 136)[et];
+      const double st_beta = q[el], st_v = q[STB + el], st_c = q[2 * STB + j];
+      const uint8_t st_code = reinterpret_cast<const uint8_t*>(q + 2 * STB + 8)[el];
       // everything that does not depend on S_J is formed before the hand-off
       const double w = st_c + k.rho * st_beta - st_v;      // eq:b_update input c + ρβ − v
       const double vr = st_v * k.inv_rho;
@@ -419,9 +505,9 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
 #pragma unroll
         for (int i = 0; i < NMW; i++) part[i] = sp[i * 64];
 #pragma unroll
-        for (int h = 1; h < NMW; h *= 2)
+        for (int hh = 1; hh < NMW; hh *= 2)
 #pragma unroll
-          for (int i = 0; i + h < NMW; i += 2 * h) part[i] += part[i + h];
+          for (int i = 0; i + hh < NMW; i += 2 * hh) part[i] += part[i + hh];
         const double sv = part[0];
         double bnz = 0.0;
         if (active) {
@@ -441,20 +527,20 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
           bnz = bn;
         }
         if (check) {
-          // append this tile's nonzeros of β⁺ to the (CTA, epilogue warp, node) segment, in column
-          // order: ballot + popcount, no barrier (every lane of a node keeps the same running count)
+          // append this tile's nonzeros of β⁺ to the (sub-range, epilogue warp, node) segment, in
+          // column order: ballot + popcount, no barrier (every lane of a node keeps the same count)
           const unsigned bal = __ballot_sync(0xffffffffu, bnz != 0.0);
           const unsigned mnode = bal & (0x01010101u << nd);
           if (bnz != 0.0) {
             const int r = seg_n + __popc(mnode & ((1u << (tid & 31)) - 1u));
-            const int64_t o = ((int64_t)(blockIdx.x * NEW + ew) * kBC + nd) * k.seg_cap + r;
+            const int64_t o = (((int64_t)sr * NEW + ew) * kBC + node) * k.seg_cap + r;
             k.seg_idx[o] = (int32_t)(col0 + j);
             k.seg_val[o] = bnz;
           }
           seg_n += __popc(mnode);
         }
       }
-      s.Ws[(m & 1) * kBC * 12 + nd * 12 + j] = wn;
+      s.Ws[(m & 1) * 8 * 12 + nd * 12 + j] = wn;
       mbar_arrive_warp(&s.wready[m & 1]);
       PROF_ACC(5);
     }
@@ -466,22 +552,17 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       }
     // β, v were written through the generic proxy; the next sweep reads them with TMA
     fence_proxy_async_global();
-    if (fused && check && (et & 31) < kBC) k.seg_cnt[(blockIdx.x * NEW + ew) * kBC + nd] = seg_n;
-    if (fused && check) {
-      // stash per-thread sums; reduced below after the CTA barrier
-      s.Ws[2 * kBC * 12 + et * 4 + 0] = sT1;
-      s.Ws[2 * kBC * 12 + et * 4 + 1] = sT2;
-      s.Ws[2 * kBC * 12 + et * 4 + 2] = sT3;
-      s.Ws[2 * kBC * 12 + et * 4 + 3] = sT4;
-    }
+    if (sr == sr0) eflush();
+    if (paired && sr == sr0 + 1) eflush();
   }
   __syncthreads();
   if (tid == 0) prefill(k, s, s.sched[0] + 1);
-  if (fused && check && tid < kBC * 4) {
-    const int nd = tid >> 2, q = tid & 3;
+  // per-sub-range check sums of the CTA's 8 nodes (fixed order over the tile's 8 columns)
+  if (fused && check && tid < (paired ? 2 : 1) * 8 * 4) {
+    const int si = tid >> 5, nd = (tid >> 2) & 7, q = tid & 3;
     double a = 0.0;
-    for (int j = 0; j < 8; j++) a += s.Ws[2 * kBC * 12 + (j * 8 + nd) * 4 + q];
-    k.sums[((int64_t)g * kBC + nd) * kSums + q] = a;
+    for (int j = 0; j < 8; j++) a += s.Ws[2 * 8 * 12 + (si * 64 + j * 8 + nd) * 4 + q];
+    k.sums[((int64_t)(sr0 + si) * kBC + 8 * h + nd) * kSums + q] = a;
   }
 }
 
@@ -492,15 +573,17 @@ constexpr int RED_E = 64;
 constexpr int RED_C = kAdmmThreads / RED_E;
 __device__ void reduce_u(const KP& k, Smem& s, double* dst) {
   const int tid = threadIdx.x;
-  const int g = blockIdx.x, G = gridDim.x;
+  const int g = blockIdx.x, G = gridDim.x, Q = k.nsr;
   const int64_t E = (int64_t)kBC * k.n8;
   const int64_t e0 = E * g / G, e1 = E * (g + 1) / G;
   const int el = tid % RED_E, c = tid / RED_E;
-  const int q0 = G * c / RED_C, q1 = G * (c + 1) / RED_C;
+  const int q0 = Q * c / RED_C, q1 = Q * (c + 1) / RED_C;
   for (int64_t eb = e0; eb < e1; eb += RED_E) {
     const int64_t e = eb + el;
     double a = 0.0;
-    if (e < e1) {
+    // inactive nodes: their partials were not written this sweep, and their u is never used
+    const bool live = e < e1 && (s.flags[e / k.n8] & F_ACTIVE);
+    if (live) {
       const int64_t nd = e / k.n8, row = e % k.n8;
       const double* src = k.Upart + nd * k.ld + row;
       const int64_t qs = (int64_t)kBC * k.ld;
@@ -509,7 +592,7 @@ __device__ void reduce_u(const KP& k, Smem& s, double* dst) {
     }
     s.spart[c * RED_E + el] = a;
     __syncthreads();
-    if (c == 0 && e < e1) {
+    if (c == 0 && live) {
       double r = s.spart[el];
 #pragma unroll
       for (int cc = 1; cc < RED_C; cc++) r += s.spart[cc * RED_E + el];
@@ -522,23 +605,27 @@ __device__ void reduce_u(const KP& k, Smem& s, double* dst) {
 
 // Dense per-node list of β⁺'s nonzeros: CTA g copies its segment to offset Σ_{g'<g} cnt[g'].
 // Returns (in tot[nd], every CTA identically) the node's total count.
-__device__ void compact_nonzeros(const KP& k, int* tot) {
-  const int g = blockIdx.x, G = gridDim.x;
+// (Active nodes only: the segments of the others were not written this sweep; their total is 0.)
+// CTA g copies the segments of sub-range g.
+__device__ void compact_nonzeros(const KP& k, Smem& s, int* tot) {
+  const int g = blockIdx.x, G = k.nsr;
   __shared__ int off_s[kBC];
   if (threadIdx.x < kBC) {
     const int nd = threadIdx.x;
     int off = 0, all = 0;
-    for (int q = 0; q < G * NEW; q++) {   // segments in (CTA, epilogue warp) order
-      const int c = __ldcg(k.seg_cnt + q * kBC + nd);
-      if (q < g * NEW) off += c;
-      all += c;
-    }
+    if (s.flags[nd] & F_ACTIVE)
+      for (int q = 0; q < G * NEW; q++) {   // segments in (sub-range, epilogue warp) order
+        const int c = __ldcg(k.seg_cnt + q * kBC + nd);
+        if (q < g * NEW) off += c;
+        all += c;
+      }
     off_s[nd] = off;
     tot[nd] = all;
   }
   __syncthreads();
   for (int w = 0; w < NEW; w++)
     for (int nd = 0; nd < kBC; nd++) {
+      if (!(s.flags[nd] & F_ACTIVE)) continue;
       const int q = g * NEW + w;
       const int c = __ldcg(k.seg_cnt + q * kBC + nd);
       int off = off_s[nd];
@@ -553,51 +640,55 @@ __device__ void compact_nonzeros(const KP& k, int* tot) {
 }
 
 // ‖Xβ‖² partials from the sparse β⁺ (nodes with ≤ nz_cap nonzeros): CTA g owns rows [i0, i1).
-// Warp pair (2·nd, 2·nd+1) serves node nd: lane l of the pair takes entries e ≡ l (mod 64) and
-// accumulates X[i, j_e]·β_e for 8 rows i at once (one contiguous 64-byte piece of column j_e);
-// the 64 slot sums are reduced by a fixed butterfly and a fixed pair order — deterministic and
-// independent of the batch.
+// In pass h, warp pair (2·nl, 2·nl+1) serves node nd = 8h + nl: lane l of the pair takes entries
+// e ≡ l (mod 64) and accumulates X[i, j_e]·β_e for 8 rows i at once (one contiguous 64-byte piece
+// of column j_e); the 64 slot sums are reduced by a fixed butterfly and a fixed pair order —
+// deterministic and independent of the batch.
 __device__ void gather_partial(const KP& k, Smem& s, const int* tot) {
   const int g = blockIdx.x, G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t i0 = k.n * g / G, i1 = k.n * (g + 1) / G;
-  const int nd = warp >> 1, slot = (warp & 1) * 32 + lane;
-  double* red = s.spart;   // [kBC][2][8]
-  const bool use = nd < kBC && (s.flags[nd] & F_ACTIVE) && tot[nd] <= k.nz_cap;
-  double part = 0.0;
-  for (int64_t r0 = i0; r0 < i1; r0 += 8) {
-    double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (use) {
-      const int cnt = tot[nd];
-      const int32_t* ix = k.nz_idx + (int64_t)nd * k.nz_cap;
-      const double* vx = k.nz_val + (int64_t)nd * k.nz_cap;
-      const int nr = (int)(i1 - r0 < 8 ? i1 - r0 : 8);
+  const int nl = warp >> 1, slot = (warp & 1) * 32 + lane;
+  double* red = s.spart;   // [8][2][8]
+  double part = 0.0;       // thread tid < kBC: node tid
+  for (int h = 0; h < NH; h++) {
+    const int nd = 8 * h + nl;
+    const bool use = nl < 8 && (s.flags[nd] & F_ACTIVE) && tot[nd] <= k.nz_cap;
+    for (int64_t r0 = i0; r0 < i1; r0 += 8) {
+      double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (use) {
+        const int cnt = tot[nd];
+        const int32_t* ix = k.nz_idx + (int64_t)nd * k.nz_cap;
+        const double* vx = k.nz_val + (int64_t)nd * k.nz_cap;
+        const int nr = (int)(i1 - r0 < 8 ? i1 - r0 : 8);
 #pragma unroll 2
-      for (int e = slot; e < cnt; e += 64) {
-        const double bv = __ldcg(vx + e);
-        const double* col = k.X + (int64_t)__ldcg(ix + e) * k.ld + r0;
+        for (int e = slot; e < cnt; e += 64) {
+          const double bv = __ldcg(vx + e);
+          const double* col = k.X + (int64_t)__ldcg(ix + e) * k.ld + r0;
 #pragma unroll
-        for (int r = 0; r < 8; r++)
-          if (r < nr) a[r] = fma(bv, __ldg(col + r), a[r]);
+          for (int r = 0; r < 8; r++)
+            if (r < nr) a[r] = fma(bv, __ldg(col + r), a[r]);
+        }
       }
-    }
 #pragma unroll
-    for (int r = 0; r < 8; r++)
+      for (int r = 0; r < 8; r++)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a[r] += __shfl_xor_sync(0xffffffffu, a[r], o);
-    if (nd < kBC && lane < 8) {
-      double v = 0.0;
+        for (int o = 16; o > 0; o >>= 1) a[r] += __shfl_xor_sync(0xffffffffu, a[r], o);
+      if (nl < 8 && lane < 8) {
+        double v = 0.0;
 #pragma unroll
-      for (int r = 0; r < 8; r++) v = lane == r ? a[r] : v;
-      red[(nd * 2 + (warp & 1)) * 8 + lane] = v;
-    }
-    __syncthreads();
-    if (tid < kBC) {
-      for (int r = 0; r < 8 && r0 + r < i1; r++) {
-        const double xb = red[(tid * 2) * 8 + r] + red[(tid * 2 + 1) * 8 + r];
-        part = fma(xb, xb, part);
+        for (int r = 0; r < 8; r++) v = lane == r ? a[r] : v;
+        red[(nl * 2 + (warp & 1)) * 8 + lane] = v;
       }
+      __syncthreads();
+      if ((tid >> 3) == h && tid < kBC) {
+        const int l = tid & 7;
+        for (int r = 0; r < 8 && r0 + r < i1; r++) {
+          const double xb = red[(l * 2) * 8 + r] + red[(l * 2 + 1) * 8 + r];
+          part = fma(xb, xb, part);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   if (tid < kBC && (s.flags[tid] & F_ACTIVE) && tot[tid] <= k.nz_cap) k.sums2[(int64_t)g * kBC + tid] = part;
 }
@@ -649,7 +740,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     s.stq = base + (size_t)NST * kPt * k.ld;
     s.spart = s.stq + NST * STQ;
     s.Ws = s.spart + 2 * NMW * 64;
-    s.red = s.Ws + 2 * kBC * 12 + 64 * 4;
+    s.red = s.Ws + 2 * 8 * 12 + 2 * 64 * 4;
     s.mbar = reinterpret_cast<uint64_t*>(s.red + kBC);
     s.sready = s.mbar + NST;
     s.wready = s.sready + 2;
@@ -676,6 +767,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   __syncthreads();
   unsigned phases = 0, hph = 0;
   if (tid == 0) prefill(k, s, 0);
+  __syncthreads();   // the sweep reads its node half and sub-ranges from s.sched
 
   // u0 = Z (c + ρβ0 − v0), then the warm/cold refresh sweep (R6)
   sweep<SW_FWD_W, KS, MT>(k, s, false, false, phases, hph);
@@ -695,7 +787,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     grid_sync(k.bar);
     reduce_u(k, s, k.U);
     __shared__ int tot_s[kBC];
-    if (chk) compact_nonzeros(k, tot_s);   // β⁺'s nonzeros → dense per-node lists
+    if (chk) compact_nonzeros(k, s, tot_s);   // β⁺'s nonzeros → dense per-node lists
     grid_sync(k.bar);
     PROF_ACC(7);
     if (!chk) continue;
@@ -937,8 +1029,8 @@ int debug_prof(unsigned long long*, int) { return 0; }
 #endif
 
 size_t admm_smem_bytes(int64_t ld) {
-  return sizeof(double) * ((size_t)NST * kPt * ld + NST * STQ + 2 * NMW * 64 + 2 * kBC * 12 + 64 * 4 + kBC) +
-         (NST + 4) * sizeof(uint64_t) + 2 * kBC * sizeof(int) + (NST + 4) * sizeof(int) + NST * sizeof(unsigned) + 64;
+  return sizeof(double) * ((size_t)NST * kPt * ld + NST * STQ + 2 * NMW * 64 + 2 * 8 * 12 + 2 * 64 * 4 + kBC) +
+         (NST + 4) * sizeof(uint64_t) + 2 * kBC * sizeof(int) + (NST + 12) * sizeof(int) + NST * sizeof(unsigned) + 64;
 }
 
 int admm_alloc(Ctx* c) {
@@ -948,8 +1040,10 @@ int admm_alloc(Ctx* c) {
     return set_err(c, L0L2_EINVAL, "n = %lld > %d not supported by the fused ADMM kernel", (long long)c->n,
                    std::min(4 * NMW * CLS_KS[NCLS - 1], 8 * NMW * CLS_MT[NCLS - 1]));
   const int ntiles = (int)(p8 / kPt);
+  // an even grid: CTA pairs (2P, 2P+1) serve the two node halves; a sub-range may be empty
   c->grid = std::min(c->sms, ntiles);
   if (const char* e = getenv("L0L2_GRID")) c->grid = std::max(1, std::min(c->grid, atoi(e)));   // testing hook
+  c->grid = std::max(2, c->grid & ~1);
   c->beta = (double*)dalloc(c, sizeof(double) * p8 * kBC);
   c->v = (double*)dalloc(c, sizeof(double) * p8 * kBC);
   c->bchk = (double*)dalloc(c, sizeof(double) * p8 * kBC);
@@ -1027,7 +1121,12 @@ int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st) {
   k.pfs = 0;
   if (const char* e = getenv("L0L2_PFS")) k.pfs = std::max(0, atoi(e));   // tuning hook
   if (const char* e = getenv("L0L2_PFD")) k.pfd = std::max(0, atoi(e));   // tuning hook
-  k.ntiles = (int)(k.p8 / kPt); k.nb = a.nb; k.check_every = c->check_every; k.max_iters = c->max_iters;
+  k.tsplit = 1;
+  if (const char* e = getenv("L0L2_TSPLIT")) {                           // tuning hook
+    const int v = atoi(e);
+    k.tsplit = (v == 2 || v == 4 || v == 8) ? v : 1;
+  }
+  k.ntiles = (int)(k.p8 / kPt); k.nsr = c->grid; k.nb = a.nb; k.check_every = c->check_every; k.max_iters = c->max_iters;
   k.rho = c->rho; k.inv_rho = 1.0 / c->rho; k.lam0 = c->lam0; k.lam2 = c->lam2; k.M = c->M; k.yy = c->yy;
   k.node_tol = c->node_tol;
   k.shrink = c->rho / (c->rho + 2.0 * c->lam2);

@@ -10,7 +10,7 @@
 
 namespace l0l2 {
 
-constexpr int kBC = 8;          // node columns per ADMM pass (DMMA n-dim = 8)
+constexpr int kBC = 16;         // node columns per ADMM pass: two DMMA n=8 halves share each Z tile
 constexpr int kPt = 8;          // Z columns per tile (DMMA m-dim of the adjoint = 8)
 constexpr int kAdmmThreads = 512;  // 16 warps per persistent CTA
 constexpr int kSums = 6;        // per-node partial sums of a check (see admm.cu)

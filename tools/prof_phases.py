@@ -12,7 +12,7 @@ from paper_2602_04551_b200 import Problem, binding  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 100
-nb = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+nb = int(sys.argv[3]) if len(sys.argv) > 3 else 16
 inst = synth.config_instance(cfg, seed=0)
 rho = 3.0 * float(np.mean(np.einsum("ij,ij->j", inst.X, inst.X)))
 pr = Problem(inst.X, inst.y, inst.lambda0, inst.lambda2, inst.M, rho=rho, node_tol=-1.0, max_iters=iters)
