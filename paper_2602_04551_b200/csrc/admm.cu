@@ -47,10 +47,9 @@ constexpr int F_ACTIVE = 8;             // internal node flag bit (not exported)
 
 struct KP {
   const double* __restrict__ Z;
-  const double* __restrict__ c;
   const double* __restrict__ Lt;   // Lᵀ, col-major ld (column i = row i of L)
-  double* beta; double* v; double* bchk;
-  const uint8_t* __restrict__ code;
+  double* stt;                     // node state in tile blocks (st_* below)
+  double* bchk;                    // b at the last check, [p][kBC]
   double* U; double* Ub; double* Upart; double* sums; double* sums2;
   // nonzeros of β⁺ at check iterations (sparse primal): per-CTA segments in tile
   // order, then a dense per-node list in CTA order
@@ -175,7 +174,10 @@ __device__ __forceinline__ double nu_f(const KP& k, double x, uint8_t code) {   
 }
 
 // ---------------------------------------------------------------- shared memory layout
-constexpr int NST = 3;         // Z tile stages in the TMA ring
+#ifndef L0L2_NST
+#define L0L2_NST 3
+#endif
+constexpr int NST = L0L2_NST;  // Z tile stages in the TMA ring (3 × 64.75 KB at n = 1000)
 constexpr int PFD_DEFAULT = 1; // additional tiles prefetched into L2 beyond the smem ring (k.pfd)
 constexpr int NMW = NW - 2;    // MMA warps (adjoint + forward); the last 2 warps run the epilogue
 constexpr int MMA_THREADS = NMW * 32;
@@ -191,8 +193,19 @@ constexpr int CLS_MT[NCLS] = {1, 3, 5, 9, 10};
 //   β_J [8][kBC], v_J [8][kBC], c_J [8], code_J [8][kBC] bytes (node-minor, as in HBM; a CTA
 //   uses its half's 8 nodes of each row)
 constexpr int STB = kPt * kBC;                             // (column, node) elements per tile
-constexpr int STQ = STB + STB + 8 + STB / 8;               // doubles per stage
-constexpr unsigned STQ_BYTES = 8 * STB + 8 * STB + 64 + STB;
+constexpr int STQ = (STB + STB + 8 + STB / 8 + 15) / 16 * 16;   // doubles per stage (128-B multiple)
+constexpr unsigned STQ_BYTES = 8 * STQ;
+// The node state lives in HBM in the same per-tile blocks ("stt", STQ doubles per 8-column tile),
+// so each stage needs ONE bulk copy for all of it:  β at st_beta(j, nd), v at st_beta(j, nd) + STB,
+// c_j at st_c(j), the fixation code byte at st_code(j, nd).
+__host__ __device__ __forceinline__ int64_t st_beta(int64_t j, int nd) { return (j >> 3) * STQ + (j & 7) * kBC + nd; }
+__host__ __device__ __forceinline__ int64_t st_c(int64_t j) { return (j >> 3) * STQ + 2 * STB + (j & 7); }
+__device__ __forceinline__ uint8_t& st_code(double* stt, int64_t j, int nd) {
+  return reinterpret_cast<uint8_t*>(stt + (j >> 3) * STQ + 2 * STB + 8)[(j & 7) * kBC + nd];
+}
+__device__ __forceinline__ uint8_t st_code(const double* stt, int64_t j, int nd) {
+  return reinterpret_cast<const uint8_t*>(stt + (j >> 3) * STQ + 2 * STB + 8)[(j & 7) * kBC + nd];
+}
 
 struct Smem {
   double* tiles;      // [NST][kPt][ld]   Z_J ring (stage q at tiles + q·kPt·ld)
@@ -231,7 +244,10 @@ enum { SW_FWD_W = 0, SW_FWD_BETA = 1, SW_FUSED = 2 };
 __device__ unsigned long long g_prof[160][NW][8];
 #define PROF_T0() long long pt_ = clock64()
 #define PROF_RESET() pt_ = clock64()
-#define PROF_ACC(slot) do { long long n_ = clock64(); if ((threadIdx.x & 31) == 0) g_prof[blockIdx.x][threadIdx.x >> 5][slot] += (unsigned long long)(n_ - pt_); pt_ = n_; } while (0)
+// per-warp totals in shared memory (a global read-modify-write per phase would distort the timing);
+// flushed to g_prof once at the end of the launch
+__shared__ unsigned long long prof_s[NW][8];
+#define PROF_ACC(slot) do { long long n_ = clock64(); if ((threadIdx.x & 31) == 0) prof_s[threadIdx.x >> 5][slot] += (unsigned long long)(n_ - pt_); pt_ = n_; } while (0)
 #else
 #define PROF_T0() do {} while (0)
 #define PROF_RESET() do {} while (0)
@@ -244,16 +260,14 @@ __device__ __forceinline__ unsigned tile_bytes(const KP& k) { return (unsigned)(
 __device__ __forceinline__ void issue_stage(const KP& k, Smem& s, int t, int sg) {
   const unsigned tb = tile_bytes(k);
   mbar_expect_tx(&s.mbar[sg], tb + STQ_BYTES);
-  // Z_J as k.tsplit bulk copies of kPt/tsplit whole columns each (more requests in flight)
+  // Z_J as k.tsplit bulk copies of kPt/tsplit whole columns each (1 is fastest: every copy issued
+  // costs the issuing MMA warp time on the critical path)
   const int cpc = kPt / k.tsplit;
   for (int c = 0; c < kPt; c += cpc)
     bulk_g2s(s.tiles + (size_t)sg * kPt * k.ld + c * k.ld, k.Z + ((int64_t)t * kPt + c) * k.ld,
              (unsigned)(cpc * k.ld * sizeof(double)), &s.mbar[sg]);
-  double* q = s.stq + sg * STQ;
-  bulk_g2s(q, k.beta + (int64_t)t * STB, 8 * STB, &s.mbar[sg]);
-  bulk_g2s(q + STB, k.v + (int64_t)t * STB, 8 * STB, &s.mbar[sg]);
-  bulk_g2s(q + 2 * STB, k.c + (int64_t)t * kPt, 64, &s.mbar[sg]);
-  bulk_g2s(q + 2 * STB + 8, k.code + (int64_t)t * STB, STB, &s.mbar[sg]);
+  // the tile's whole state block (β_J, v_J, c_J, code_J) in one copy
+  bulk_g2s(s.stq + sg * STQ, k.stt + (int64_t)t * STQ, STQ_BYTES, &s.mbar[sg]);
 }
 
 // Tile scheduling.  Every sweep streams all tiles of Z once.  Sub-range r < G = gridDim.x is
@@ -356,10 +370,13 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
   };
 
   if (is_mma) {
-    // Branch-free fragment schedule (so every shared-memory fragment load can be hoisted ahead of
-    // its DMMA): warp w owns adjoint k-steps q = w + NMW·i (i < KS) and forward row tiles
-    // m = w + NMW·i (i < MT); indices past the end are clamped to a valid row (their u fragment is
-    // 0, their forward accumulator is never stored).
+    // Branch-free fragment schedule (so every shared-memory fragment load is an immediate offset
+    // from one base and can be hoisted ahead of its DMMA): warp w owns adjoint k-steps q = w + NMW·i
+    // (i < KS) and forward row tiles m = w + NMW·i (i < MT).  Indices past n8 read rows beyond the
+    // column (Z's zero padding, the next column, or — past the ring — the staged state blocks): their
+    // u fragment is 0 and their forward accumulator is never stored.  Those reads must be finite
+    // (NaN·0 = NaN), so the ring and the state stages are zeroed at launch (stale shared memory of
+    // an earlier kernel could hold any bit pattern) and only ever receive Z and state blocks.
     const int mt = (int)(k.n8 / 8);
     const int kt = (int)(k.n8 / 4);
     const int ld = (int)k.ld;
@@ -401,7 +418,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       const double* T = s.tiles + (size_t)(m % NST) * kPt * ld + cA * ld + kA;
       double sc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-      for (int i = 0; i < KS; i++) dmma(sc[i & 3], T[4 * min(warp + NMW * i, kt - 1)], uf[i]);
+      for (int i = 0; i < KS; i++) dmma(sc[i & 3], T[4 * (warp + NMW * i)], uf[i]);
       double* sp = s.spart + (m & 1) * NMW * 64 + warp * 64;
       // C fragment: row (col j) = lane>>2, cols (node) = 2*(lane&3) + {0,1}
       sp[cA * 8 + 2 * kA] = (sc[0][0] + sc[1][0]) + (sc[2][0] + sc[3][0]);
@@ -428,7 +445,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       const double b1 = W[cA * 12 + 4 + kA];
 #pragma unroll
       for (int i = 0; i < MT; i++) {
-        const int row = 8 * min(warp + NMW * i, mt - 1);
+        const int row = 8 * (warp + NMW * i);
         dmma(acc[i], T[row], b0);                // A[m = row][k = col j]
         dmma(acc[i], T[4 * ld + row], b1);
       }
@@ -484,13 +501,13 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       const int el = j * kBC + node;
       const int64_t e = col0 * kBC + el;
       const double* q = s.stq + sg * STQ;
-      const double st_beta = q[el], st_v = q[STB + el], st_c = q[2 * STB + j];
-      const uint8_t st_code = reinterpret_cast<const uint8_t*>(q + 2 * STB + 8)[el];
+      const double q_beta = q[el], q_v = q[STB + el], q_c = q[2 * STB + j];
+      const uint8_t q_code = reinterpret_cast<const uint8_t*>(q + 2 * STB + 8)[el];
       // everything that does not depend on S_J is formed before the hand-off
-      const double w = st_c + k.rho * st_beta - st_v;      // eq:b_update input c + ρβ − v
-      const double vr = st_v * k.inv_rho;
+      const double w = q_c + k.rho * q_beta - q_v;      // eq:b_update input c + ρβ − v
+      const double vr = q_v * k.inv_rho;
       double wn = 0.0;
-      if (!fused && active) wn = (MODE == SW_FWD_BETA) ? st_beta : w;
+      if (!fused && active) wn = (MODE == SW_FWD_BETA) ? q_beta : w;
       PROF_ACC(1);
       // fused: S_J(m) partials written; forward-only: w⁺ buffer m&1 released by fwd(m − 2)
       if (fused || m >= 2) {
@@ -512,18 +529,18 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
         double bnz = 0.0;
         if (active) {
           const double b = (w - sv) * k.inv_rho;               // b = D w, D = (I − ZᵀZ)/ρ (R1)
-          const double bn = refresh ? st_beta : prox(k, b + vr, st_code);
-          const double vn = st_v + k.rho * (b - bn);
+          const double bn = refresh ? q_beta : prox(k, b + vr, q_code);
+          const double vn = q_v + k.rho * (b - bn);
           if (check) {
             sT1 = fma(b, sv, sT1);
-            sT2 += nu_f(k, fabs(st_c - sv), st_code);
-            sT3 = fma(st_c, bn, sT3);
-            sT4 += psi_f(k, bn, st_code);
+            sT2 += nu_f(k, fabs(q_c - sv), q_code);
+            sT3 = fma(q_c, bn, sT3);
+            sT4 += psi_f(k, bn, q_code);
             k.bchk[e] = b;
           }
-          k.beta[e] = bn;
-          k.v[e] = vn;
-          wn = st_c + k.rho * bn - vn;
+          k.stt[st_beta(col0 + j, node)] = bn;
+          k.stt[st_beta(col0 + j, node) + STB] = vn;
+          wn = q_c + k.rho * bn - vn;
           bnz = bn;
         }
         if (check) {
@@ -760,11 +777,15 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < NST) s.rel[tid] = 0;
+  for (size_t i = tid; i < (size_t)NST * kPt * k.ld + NST * STQ; i += blockDim.x) s.tiles[i] = 0.0;   // stq follows
   if (tid < kBC) {
     s.flags[tid] = __ldcg(k.nodei + tid * 2);
     s.red[tid] = -INFINITY;
   }
   __syncthreads();
+#ifdef L0L2_PROF
+  if (tid < NW * 8) prof_s[tid / 8][tid % 8] = 0;
+#endif
   unsigned phases = 0, hph = 0;
   if (tid == 0) prefill(k, s, 0);
   __syncthreads();   // the sweep reads its node half and sub-ranges from s.sched
@@ -843,6 +864,10 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     for (int nd = 0; nd < kBC; nd++) any |= s.flags[nd] & F_ACTIVE;
     if (!any) break;
   }
+#ifdef L0L2_PROF
+  __syncthreads();
+  if (tid < NW * 8) g_prof[blockIdx.x][tid / 8][tid % 8] += prof_s[tid / 8][tid % 8];
+#endif
   // drain the prefill issued after the last sweep before the CTA retires
   if (tid == 0)
     for (int sg = 0; sg < NST && sg < s.sched[1]; sg++) mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
@@ -859,25 +884,26 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
 // ---------------------------------------------------------------- packing / finalize kernels
 
 // code plane and state for one group: column j, node nd (nd ≥ nb and j ≥ p are inactive F0)
-__global__ void pack_kernel(int64_t p, int64_t p8, int nb, uint8_t* code, double* beta, double* v,
+__global__ void pack_kernel(int64_t p, int64_t p8, int nb, double* stt, const double* __restrict__ c,
                             const double* const* warm) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= p8 * kBC) return;
   const int64_t j = e / kBC;
   const int nd = (int)(e % kBC);
   uint8_t cd = (nd < nb && j < p) ? 0 : 1;
-  code[e] = cd;
+  st_code(stt, j, nd) = cd;
   double b = 0.0, vv = 0.0;
   if (nd < nb && j < p && warm != nullptr && warm[nd] != nullptr) {
     b = warm[nd][j];
     vv = warm[nd][p + j];
   }
-  beta[e] = b;
-  v[e] = vv;
+  stt[st_beta(j, nd)] = b;
+  stt[st_beta(j, nd) + STB] = vv;
+  if (nd == 0) stt[st_c(j)] = j < p ? c[j] : 0.0;
 }
 
 __global__ void scatter_fix(int nb, const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
-                            const uint8_t* __restrict__ val, uint8_t* code, double* beta, int64_t p, int* bad) {
+                            const uint8_t* __restrict__ val, double* stt, int64_t p, int* bad) {
   const int nd = blockIdx.x;
   if (nd >= nb) return;
   const int64_t q0 = off[nd], q1 = off[nd + 1];
@@ -887,9 +913,8 @@ __global__ void scatter_fix(int nb, const int64_t* __restrict__ off, const int32
     const uint8_t cd = val[q] ? 2 : 1;
     for (int64_t r = q0; r < q; r++)               // F0 ∩ F1 ≠ ∅, order independent
       if (idx[r] == j && (val[r] ? 2 : 1) != cd) atomicOr(bad, 2);
-    const int64_t e = (int64_t)j * kBC + nd;
-    code[e] = cd;
-    if (cd == 1) beta[e] = 0.0;                    // warm edit: β_j ← 0 on F0
+    st_code(stt, j, nd) = cd;
+    if (cd == 1) stt[st_beta(j, nd)] = 0.0;        // warm edit: β_j ← 0 on F0
   }
 }
 
@@ -913,7 +938,7 @@ __device__ __forceinline__ bool better(const BrKey& a, const BrKey& b) {
 }
 
 __global__ void __launch_bounds__(512) finalize_kernel(int64_t p, double M, double zsr, bool lam0_pos, double int_tol,
-                                                       const double* __restrict__ beta, const uint8_t* __restrict__ code,
+                                                       const double* __restrict__ stt,
                                                        double* zhat, int64_t ldz, int32_t* branch_j, uint8_t* flags,
                                                        int32_t* supp_cnt, int32_t* supp_idx, int64_t supp_stride) {
   const int nd = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -929,8 +954,8 @@ __global__ void __launch_bounds__(512) finalize_kernel(int64_t p, double M, doub
     const int64_t j = c0 + tid;
     bool insupp = false;
     if (j < p) {
-      const double b = beta[j * kBC + nd];
-      const uint8_t cd = code[j * kBC + nd];
+      const double b = stt[st_beta(j, nd)];
+      const uint8_t cd = st_code(stt, j, nd);
       const double ab = fabs(b);
       double z;
       if (cd == 1) z = 0.0;
@@ -980,15 +1005,14 @@ __global__ void __launch_bounds__(512) finalize_kernel(int64_t p, double M, doub
   }
 }
 
-__global__ void unpack_kernel(int64_t p, int nb, const double* __restrict__ beta, const double* __restrict__ v,
-                              double* const* warm) {
+__global__ void unpack_kernel(int64_t p, int nb, const double* __restrict__ stt, double* const* warm) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= p * kBC) return;
   const int64_t j = e / kBC;
   const int nd = (int)(e % kBC);
   if (nd >= nb || warm[nd] == nullptr) return;
-  warm[nd][j] = beta[e];
-  warm[nd][p + j] = v[e];
+  warm[nd][j] = stt[st_beta(j, nd)];
+  warm[nd][p + j] = stt[st_beta(j, nd) + STB];
 }
 
 __global__ void fill_y(double* r, int64_t ldr, const double* y, int64_t n, int nb) {
@@ -1044,10 +1068,9 @@ int admm_alloc(Ctx* c) {
   c->grid = std::min(c->sms, ntiles);
   if (const char* e = getenv("L0L2_GRID")) c->grid = std::max(1, std::min(c->grid, atoi(e)));   // testing hook
   c->grid = std::max(2, c->grid & ~1);
-  c->beta = (double*)dalloc(c, sizeof(double) * p8 * kBC);
-  c->v = (double*)dalloc(c, sizeof(double) * p8 * kBC);
+  c->stt = (double*)dalloc(c, sizeof(double) * (p8 / kPt) * STQ);
+  if (c->stt) L0L2_CUDA(c, cudaMemset(c->stt, 0, sizeof(double) * (p8 / kPt) * STQ));   // padding stays 0
   c->bchk = (double*)dalloc(c, sizeof(double) * p8 * kBC);
-  c->code = (uint8_t*)dalloc(c, p8 * kBC);
   c->U = (double*)dalloc(c, sizeof(double) * kBC * ld);
   c->Ub = (double*)dalloc(c, sizeof(double) * kBC * ld);
   c->Upart = (double*)dalloc(c, sizeof(double) * c->grid * kBC * ld);
@@ -1068,7 +1091,7 @@ int admm_alloc(Ctx* c) {
   c->node_i = (int*)dalloc(c, sizeof(int) * kBC * 2);
   c->bar = (unsigned*)dalloc(c, sizeof(unsigned) * 2);
   c->badflag = (int*)dalloc(c, sizeof(int));
-  if (!c->beta || !c->v || !c->bchk || !c->code || !c->U || !c->Ub || !c->Upart || !c->sums || !c->sums2 ||
+  if (!c->stt || !c->bchk || !c->U || !c->Ub || !c->Upart || !c->sums || !c->sums2 ||
       !c->node_f || !c->node_i || !c->bar || !c->badflag)
     return set_err(c, L0L2_ENOMEM, "admm work space");
   L0L2_CUDA(c, cudaMemset(c->U, 0, sizeof(double) * kBC * ld));
@@ -1089,11 +1112,11 @@ int pack_group(Ctx* c, int nb, const int64_t* fix_off, const int32_t* fix_idx, c
                const double* const* warm_ptrs_dev, cudaStream_t st) {
   const int64_t p8 = round8(c->p);
   const int64_t tot = p8 * kBC;
-  pack_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->p, p8, nb, c->code, c->beta, c->v, warm_ptrs_dev);
+  pack_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->p, p8, nb, c->stt, c->c, warm_ptrs_dev);
   L0L2_LAUNCHED(c);
   if (fix_off) {
     L0L2_CUDA(c, cudaMemsetAsync(c->badflag, 0, sizeof(int), st));
-    scatter_fix<<<nb, 128, 0, st>>>(nb, fix_off, fix_idx, fix_val, c->code, c->beta, c->p, c->badflag);
+    scatter_fix<<<nb, 128, 0, st>>>(nb, fix_off, fix_idx, fix_val, c->stt, c->p, c->badflag);
     L0L2_LAUNCHED(c);
     int bad = 0;
     L0L2_CUDA(c, cudaMemcpyAsync(&bad, c->badflag, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1108,8 +1131,8 @@ int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st) {
   init_nodes<<<1, 32, 0, st>>>(a.nb, a.parent_lb, c->node_f, c->node_i);
   L0L2_LAUNCHED(c);
   KP k{};
-  k.Z = c->Z; k.c = c->c; k.Lt = c->Lt;
-  k.beta = c->beta; k.v = c->v; k.bchk = c->bchk; k.code = c->code;
+  k.Z = c->Z; k.Lt = c->Lt;
+  k.stt = c->stt; k.bchk = c->bchk;
   k.U = c->U; k.Ub = c->Ub; k.Upart = c->Upart; k.sums = c->sums; k.sums2 = c->sums2;
   k.nodef = c->node_f; k.nodei = c->node_i; k.bar = c->bar;
   k.seg_idx = c->seg_idx; k.seg_val = c->seg_val; k.seg_cnt = c->seg_cnt; k.nz_idx = c->nz_idx; k.nz_val = c->nz_val;
@@ -1170,7 +1193,7 @@ int finalize_group(Ctx* c, int nb, double* zhat, int32_t* branch_j, uint8_t* fla
                    int32_t* supp_idx, int64_t supp_stride, cudaStream_t st) {
   const bool lam0_pos = c->lam0 > 0.0;
   const double zsr = lam0_pos ? std::sqrt(c->lam2 / c->lam0) : 0.0;
-  finalize_kernel<<<nb, 512, 0, st>>>(c->p, c->M, zsr, lam0_pos, c->int_tol, c->beta, c->code, zhat, c->p,
+  finalize_kernel<<<nb, 512, 0, st>>>(c->p, c->M, zsr, lam0_pos, c->int_tol, c->stt, zhat, c->p,
                                       branch_j, flags, supp_cnt, supp_idx, supp_stride);
   L0L2_LAUNCHED(c);
   return L0L2_OK;
@@ -1178,7 +1201,7 @@ int finalize_group(Ctx* c, int nb, double* zhat, int32_t* branch_j, uint8_t* fla
 
 int unpack_warm(Ctx* c, int nb, double* const* warm_ptrs_dev, cudaStream_t st) {
   const int64_t tot = c->p * kBC;
-  unpack_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->p, nb, c->beta, c->v, warm_ptrs_dev);
+  unpack_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->p, nb, c->stt, warm_ptrs_dev);
   L0L2_LAUNCHED(c);
   return L0L2_OK;
 }

@@ -40,8 +40,8 @@ struct Ctx {
   // device data (owned)
   double *X = nullptr, *Z = nullptr, *y = nullptr, *c = nullptr, *colsq = nullptr, *L = nullptr, *Lt = nullptr;
   // ADMM work space for one pass of kBC nodes
-  double *beta = nullptr, *v = nullptr, *bchk = nullptr;   // [p][kBC]
-  uint8_t* code = nullptr;                                  // [p][kBC]
+  double *stt = nullptr;                                    // node state, per-tile blocks (admm.cu)
+  double *bchk = nullptr;                                   // [p][kBC]
   double *U = nullptr, *Ub = nullptr;                       // [kBC][ld]
   double *Upart = nullptr;                                  // [grid][kBC][ld]
   double *sums = nullptr;                                   // [grid][kBC][kSums]

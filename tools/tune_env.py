@@ -13,7 +13,12 @@ sys.path.insert(0, ".")
 import synth
 from paper_2602_04551_b200 import Problem
 cfg, B, iters = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
-inst = synth.config_instance(cfg, seed=0)
+if cfg.startswith("n"):   # e.g. n500p100000: synthetic shape for kernel timing only
+    nn, pp = cfg[1:].split("p")
+    inst = synth.make_instance(int(nn), int(pp), 10, 0.1, 5.0, 0)
+    inst.lambda0, inst.lambda2, inst.M = 10.0, 0.01, 2.0
+else:
+    inst = synth.config_instance(cfg, seed=0)
 rho = 3.0 * float(np.mean(np.einsum("ij,ij->j", inst.X, inst.X)))
 pr = Problem(np.asfortranarray(inst.X), inst.y, inst.lambda0, inst.lambda2, inst.M, rho=rho, node_tol=-1.0, max_iters=iters)
 fx = [((), ())] + synth.random_fixings(inst.p, B - 1, seed=11, depth_lo=5, depth_hi=10, prefer=inst.support_true)
