@@ -274,26 +274,24 @@ __device__ __forceinline__ void issue_stage(const KP& k, Smem& s, int t, int sg)
 // the fixed tile range [T(r), T(r+1)), T(r) = ⌊ntiles·r/G⌋ (bitwise deterministic, independent of
 // the batch composition).  The CTA streams one contiguous range per sweep (set by prefill: its own
 // sub-range, or its pair's two).  The stages a CTA consumes are numbered m = 0, 1, ... in ring
-// order (slot m % NST); one thread issues each (issue_next).  After the CTA's last tile one
-// end-marker stage (tile −1, a plain arrive, no copy) is issued and consumers stop at it.  The tile
-// id is written before the (release) arrive, so every consumer reads it after its (acquire) wait on
-// the stage's mbarrier.  (A dynamic, grid-wide ticket schedule was measured and gave nothing.)
+// order (slot m % NST): stage m holds tile t0 + m while m < t1 − t0, then one end-marker stage (tile
+// −1, a plain arrive, no copy) at which consumers stop; nothing is issued past it.  Stage m is a
+// function of m alone (issue_stage_m), so the thread that refills a slot needs no shared scheduler
+// state.  The tile id is written before the (release) arrive, so every consumer reads it after its
+// (acquire) wait on the stage's mbarrier.  (A dynamic, grid-wide ticket schedule was measured and
+// gave nothing.)
 __device__ __forceinline__ int sub_t(const KP& k, int r) { return (int)((int64_t)k.ntiles * r / k.nsr); }
 
-__device__ void issue_next(const KP& k, Smem& s) {
-  if (s.sched[3]) return;
-  const int t0 = s.sched[6], t1 = s.sched[7];
-  const int sg = s.sched[1] % NST;
-  const int tile = t0 + s.sched[2] < t1 ? t0 + s.sched[2] : -1;
+__device__ void issue_stage_m(const KP& k, Smem& s, int m, int t0, int t1) {
+  if (m > t1 - t0) return;
+  const int sg = m % NST;
+  const int tile = m < t1 - t0 ? t0 + m : -1;
   s.stile[sg] = tile;
-  s.sched[1]++;
   if (tile >= 0) {
-    s.sched[2]++;
     fence_proxy_async_smem();
     issue_stage(k, s, tile, sg);
     if (k.pfd > 0 && tile + k.pfd < t1) prefetch_l2(k.Z + (int64_t)(tile + k.pfd) * kPt * k.ld, tile_bytes(k));
   } else {
-    s.sched[3] = 1;
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(&s.mbar[sg])) : "memory");
   }
 }
@@ -309,7 +307,7 @@ __device__ void issue_next(const KP& k, Smem& s) {
 // changes, those rows may have been written by the partner CTA, which may still be sweeping: the
 // issue is deferred (sched[8]) to the start of the next sweep, which follows a grid barrier.
 __device__ void issue_first(const KP& k, Smem& s) {
-  for (int m = 0; m < NST; m++) issue_next(k, s);
+  for (int m = 0; m < NST; m++) issue_stage_m(k, s, m, s.sched[6], s.sched[7]);
   // the grid reduction that follows leaves HBM idle: pull the sweep's next tiles into L2 meanwhile
   const int t0 = s.sched[6], t1 = s.sched[7];
   for (int t = t0 + NST + k.pfd; t < t1 && t < t0 + NST + k.pfs; t++) prefetch_l2(k.Z + (int64_t)t * kPt * k.ld, tile_bytes(k));
@@ -330,9 +328,8 @@ __device__ void prefill(const KP& k, Smem& s, int sw) {
   s.sched[6] = paired ? sub_t(k, g & ~1) : sub_t(k, g);
   s.sched[7] = paired ? sub_t(k, (g & ~1) + 2) : sub_t(k, g + 1);
   s.sched[0] = sw;
-  s.sched[1] = 0;
-  s.sched[2] = 0;
-  s.sched[3] = 0;
+  // stages issued now and not yet consumed (waited for by the drain at the end of the launch)
+  s.sched[1] = changed ? 0 : min(NST, s.sched[7] - s.sched[6] + 1);
   s.sched[8] = changed;
   if (!changed) issue_first(k, s);
 }
@@ -356,6 +353,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
   const bool paired = s.sched[5] != 0;
   const int sr0 = paired ? (g & ~1) : g;
   const int tb = paired ? sub_t(k, sr0 + 1) : 0x7fffffff;   // first tile of the second sub-range
+  const int t0s = s.sched[6], t1s = s.sched[7];               // this sweep's tile range
   if (s.sched[8]) {   // deferred by a mode change (prefill); a grid barrier has passed.  (sched[8]
                       // is rewritten only by the next prefill, so every thread takes this branch.)
     if (tid == 0) issue_first(k, s);
@@ -451,16 +449,17 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       }
       PROF_ACC(3);
       if (!fused) mbar_arrive_warp(&s.sready[m & 1]);   // w⁺ buffer m&1 free again
-      // release stage m: the last MMA warp to finish its forward refills the slot (no CTA barrier;
-      // acq_rel orders the scheduler state (s.sched) between successive issuing lanes).  (Issuing
-      // from an epilogue warp instead was measured slower: the refill then waits for the epilogue.)
+      // release stage m: the last MMA warp to finish its forward refills the slot with stage m + NST
+      // (no CTA barrier, no shared scheduler state: a relaxed counter suffices; the reset is ordered
+      // before the next use of the counter by the refill's release-arrive on the stage mbarrier).
+      // (Issuing from an epilogue warp instead was measured slower: the refill then waits for it.)
       __syncwarp();
       if (lane == 0) {
         unsigned old;
-        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(saddr(&s.rel[sg])) : "memory");
+        asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(saddr(&s.rel[sg])) : "memory");
         if (old == NMW - 1) {
           s.rel[sg] = 0;
-          issue_next(k, s);
+          issue_stage_m(k, s, m + NST, t0s, t1s);
         }
       }
       __syncwarp();
