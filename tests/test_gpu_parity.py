@@ -119,6 +119,22 @@ def test_batched_equals_single_bitwise(case):
     prob.close()
 
 
+def test_paired_equals_split_bitwise(case, monkeypatch):
+    """A 16-node group on paired CTAs (both node halves stream the same tiles, halves retire at
+    their own checks, the mode switches to single-half mid-launch) gives bitwise the results of the
+    same group run as two single-half launches (L0L2_PAIR=0)."""
+    name, inst, lam0, lam2, M, P = case
+    prob = Problem(inst.X, inst.y, lam0, lam2, M, rho=P.rho, node_tol=1e-6, max_iters=600)
+    fx = _fixings(inst, 16, seed=5)
+    monkeypatch.setenv("L0L2_PAIR", "1")
+    paired = prob.l0l2_bound_batch(fx)
+    monkeypatch.setenv("L0L2_PAIR", "0")
+    split = prob.l0l2_bound_batch(fx)
+    for key in ("warm_out", "lb", "primal", "iters", "branch_j", "flags"):
+        assert torch.equal(paired[key], split[key]), key
+    prob.close()
+
+
 def test_converged_bounds_and_decisions(case):
     """T3: converged LB / primal within 1e-6; LB ≤ independent relaxation optimum; iteration
     counts, branch index and support equal where the decisions are separated."""
