@@ -32,7 +32,8 @@ __all__ = [
     "FREE", "FIX0", "FIX1", "T", "psi", "h", "nu", "prox_beta", "recover_z",
     "Problem", "make_code", "primal_value", "dual_value", "admm_node", "NodeResult",
     "box_ridge", "upper_bound", "brute_force", "relaxation_fista", "bnb_solve",
-    "ub_objective", "default_rho",
+    "ub_objective", "default_rho", "MPResult", "mp_forward_scores", "mp_backward_scores",
+    "matching_pursuit",
 ]
 
 
@@ -499,3 +500,82 @@ def bnb_solve(P: Problem, B=1, gap_tol=1e-2, node_tol=1e-4, check_every=10, max_
     return dict(obj=UB, beta=beta, support=inc_S, lb=LB, gap=gap, nodes=nodes, rounds=rounds,
                 node_iters=node_iters, status=status, open=len(open_nodes), trace=trace,
                 time=time.perf_counter() - t0)
+
+
+# ----------------------------------------------------------------------------------------------
+# Matching-pursuit root heuristic (Algorithm 3; outline P:781-783)
+# ----------------------------------------------------------------------------------------------
+
+def mp_forward_scores(P: Problem, r, inS):
+    """Forward step 1(a)-(c) of Algorithm 3 for every candidate j ∉ S:
+    c = X_{S^c}ᵀ r, D = ‖X_{S^c}‖² + 2λ2, β* = c / D, β = Proj_[−M,M](β*),
+    Δ = −β⊙c + ½β²⊙D + λ0.  Members of S get Δ = +∞.  Returns (Δ, β)."""
+    c = P.X.T @ r
+    D = np.einsum("ij,ij->j", P.X, P.X) + 2.0 * P.lam2
+    b = np.clip(c / D, -P.M, P.M)
+    delta = -b * c + 0.5 * b * b * D + P.lam0
+    delta = np.where(inS, np.inf, delta)
+    return delta, b
+
+
+def mp_backward_scores(P: Problem, r, beta, S):
+    """Backward step 2(a)-(b) of Algorithm 3 for j ∈ S (in the order of S):
+    c_S = X_Sᵀ r, Δ = β⊙c_S + (½‖X_S‖² − λ2)⊙β² − λ0."""
+    S = np.asarray(S, dtype=np.int64)
+    XS = P.X[:, S]
+    cS = XS.T @ r
+    bS = beta[S]
+    return bS * cS + (0.5 * np.einsum("ij,ij->j", XS, XS) - P.lam2) * bS * bS - P.lam0
+
+
+@dataclass
+class MPResult:
+    support: np.ndarray           # sorted column indices of S
+    beta: np.ndarray              # length p, zero off S
+    obj: float                    # ½‖y − Xβ‖² + λ2‖β‖² + λ0|S| (a feasible point of eq:perspective)
+    rounds: int
+    steps: list = field(default_factory=list)   # ("+"/"−", j, Δ_j) in the order taken
+
+
+def matching_pursuit(P: Problem, max_rounds=None):
+    """Algorithm 3, step by step.  S ← ∅, β ← 0, r ← y; repeat { forward: the
+    candidate j* = argmin Δ over j ∉ S joins S if Δ_j* < 0 (β_j* ← its projected value,
+    r ← r − X_j*β_j*); backward: with the residual after the forward step, j* = argmin Δ over
+    j ∈ S leaves S if Δ_j* < 0 (r ← r + X_j*β_j*, β_j* ← 0) } until a round changes nothing.
+    Readings (R15): argmin ties → lowest column index; a round is one forward then
+    one backward step; the loop is capped at max_rounds (default 4p + 10: every accepted step
+    lowers the objective strictly, so the cap is a guard, not a stopping rule)."""
+    p = P.p
+    max_rounds = 4 * p + 10 if max_rounds is None else int(max_rounds)
+    beta = np.zeros(p)
+    r = P.y.copy()
+    inS = np.zeros(p, dtype=bool)
+    steps = []
+    rounds = 0
+    while rounds < max_rounds:
+        rounds += 1
+        changed = False
+        delta, b = mp_forward_scores(P, r, inS)
+        j = int(np.argmin(delta))            # first minimum = lowest index (R15)
+        if delta[j] < 0:
+            inS[j] = True
+            beta[j] = b[j]
+            r = r - P.X[:, j] * b[j]
+            steps.append(("+", j, float(delta[j])))
+            changed = True
+        S = np.nonzero(inS)[0]               # ascending, so argmin ties → lowest index
+        if len(S):
+            dS = mp_backward_scores(P, r, beta, S)
+            i = int(np.argmin(dS))
+            if dS[i] < 0:
+                j = int(S[i])
+                r = r + P.X[:, j] * beta[j]
+                steps.append(("-", j, float(dS[i])))
+                beta[j] = 0.0
+                inS[j] = False
+                changed = True
+        if not changed:
+            break
+    S = np.nonzero(inS)[0]
+    obj = 0.5 * float(r @ r) + P.lam2 * float(beta @ beta) + P.lam0 * len(S)
+    return MPResult(support=S, beta=beta, obj=obj, rounds=rounds, steps=steps)

@@ -404,3 +404,106 @@ def test_generator_recipe():
     C = np.cov(big.X, rowvar=False)
     off = C[~np.eye(6, dtype=bool)]
     assert abs(off.mean() - 0.2) < 0.03 and abs(np.diag(C).mean() - 1.0) < 0.03
+
+
+# ---------------------------------------------------------------- matching pursuit (Algorithm 3)
+def _F(P, beta):
+    """The objective Algorithm 3 descends, evaluated from its definition:
+    ½‖y − Xβ‖² + λ2‖β‖² + λ0·|supp β|."""
+    r = P.y - P.X @ beta
+    return 0.5 * float(r @ r) + P.lam2 * float(beta @ beta) + P.lam0 * int(np.count_nonzero(beta))
+
+
+def _mp_instance(seed, n=30, p=12):
+    inst = synth.make_instance(n, p, 3, 0.3, 4.0, seed)
+    return O.Problem(inst.X, inst.y, 2.0, 0.05, 1.5)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_mp_forward_delta_is_the_objective_change(seed):
+    """Δ_j of the forward step = F(β + β_j e_j) − F(β) for j ∉ S, at a random feasible β,
+    and β_j is the 1-D argmin over [−M, M] of ½‖r − X_j t‖² + λ2 t² (scipy)."""
+    P = _mp_instance(seed)
+    rng = np.random.default_rng(seed)
+    S = rng.choice(P.p, 4, replace=False)
+    beta = np.zeros(P.p)
+    beta[S] = rng.uniform(-P.M, P.M, 4)
+    r = P.y - P.X @ beta
+    inS = np.zeros(P.p, dtype=bool)
+    inS[S] = True
+    delta, b = O.mp_forward_scores(P, r, inS)
+    for j in np.nonzero(~inS)[0]:
+        bj = beta.copy()
+        bj[j] = b[j]
+        assert delta[j] == pytest.approx(_F(P, bj) - _F(P, beta), rel=1e-10, abs=1e-9)
+        ref = minimize_scalar(lambda t: 0.5 * np.sum((r - P.X[:, j] * t) ** 2) + P.lam2 * t * t,
+                              bounds=(-P.M, P.M), method="bounded", options={"xatol": 1e-12})
+        assert b[j] == pytest.approx(ref.x, abs=1e-7)
+    assert np.all(np.isinf(delta[S]))
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_mp_backward_delta_is_the_objective_change(seed):
+    """Δ_j of the backward step = F(β − β_j e_j) − F(β) for j ∈ S."""
+    P = _mp_instance(seed)
+    rng = np.random.default_rng(10 + seed)
+    S = np.sort(rng.choice(P.p, 5, replace=False))
+    beta = np.zeros(P.p)
+    beta[S] = rng.uniform(-P.M, P.M, 5)
+    r = P.y - P.X @ beta
+    dS = O.mp_backward_scores(P, r, beta, S)
+    for i, j in enumerate(S):
+        bj = beta.copy()
+        bj[j] = 0.0
+        assert dS[i] == pytest.approx(_F(P, bj) - _F(P, beta), rel=1e-10, abs=1e-9)
+
+
+def test_mp_orthogonal_design_is_exact():
+    """With orthogonal columns the ℓ0-ℓ2 box problem separates, so Algorithm 3 (forward steps only;
+    every backward Δ is then −(forward Δ) > 0) reaches the brute-force optimum exactly."""
+    rng = np.random.default_rng(7)
+    for trial in range(4):
+        n, p = 20, 8
+        Qm, _ = np.linalg.qr(rng.standard_normal((n, p)))
+        X = Qm * rng.uniform(0.5, 3.0, p)
+        y = X @ (rng.standard_normal(p) * rng.integers(0, 2, p)) + 0.3 * rng.standard_normal(n)
+        P = O.Problem(X, y, 0.2 + 0.2 * trial, 0.1, 1.2)
+        mp = O.matching_pursuit(P)
+        bf_obj, bf_S, _ = O.brute_force(P)
+        assert mp.obj == pytest.approx(bf_obj, rel=1e-12)
+        assert list(mp.support) == list(bf_S)
+        assert all(kind == "+" for kind, _, _ in mp.steps)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_mp_descent_fixed_point_and_valid_upper_bound(seed):
+    """Every accepted step lowers F by exactly its Δ < 0; the output is a fixed point (no forward
+    or backward Δ < 0), feasible (|β| ≤ M), F(β) = the returned objective = ub_objective on its
+    support, and never below the brute-force optimum."""
+    P = _mp_instance(seed)
+    mp = O.matching_pursuit(P)
+    beta = np.zeros(P.p)
+    inS = np.zeros(P.p, dtype=bool)
+    f = _F(P, beta)
+    # replay the step log from the definition
+    for kind, j, d in mp.steps:
+        assert d < 0
+        r = P.y - P.X @ beta
+        if kind == "+":
+            delta, b = O.mp_forward_scores(P, r, inS)
+            beta[j], inS[j] = b[j], True
+        else:
+            beta[j], inS[j] = 0.0, False
+        f_new = _F(P, beta)
+        assert f_new - f == pytest.approx(d, rel=1e-9, abs=1e-9)
+        f = f_new
+    assert np.allclose(beta, mp.beta, rtol=1e-12, atol=1e-14)   # replay recomputes r from scratch
+    assert mp.obj == pytest.approx(_F(P, mp.beta), rel=1e-12)
+    assert mp.obj == pytest.approx(O.ub_objective(P, mp.support, mp.beta[mp.support]), rel=1e-12)
+    assert np.all(np.abs(mp.beta) <= P.M)
+    r = P.y - P.X @ mp.beta
+    delta, _ = O.mp_forward_scores(P, r, np.isin(np.arange(P.p), mp.support))
+    assert np.min(delta) >= 0
+    if len(mp.support):
+        assert np.min(O.mp_backward_scores(P, r, mp.beta, mp.support)) >= 0
+    assert mp.obj >= O.brute_force(P)[0] - 1e-9
