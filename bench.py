@@ -352,6 +352,16 @@ def main():
                  "alg_bytes_per_launch": per_launch_bytes,
                  "alg_flops_per_launch": ks["admm_flops_alg"] / max(1, ks["admm_launches"]),
                  "share_of_step": ks["admm_ms"] / max(1e-9, ms / world if world > 1 else ms)})
+    # root heuristic (Algorithm 3) on the same resident X: rounds × one X scan
+    mp = None
+    if world == 1:
+        prob.l0l2_matching_pursuit()   # warm-up
+        t = time.perf_counter()
+        m = prob.l0l2_matching_pursuit()
+        dt = time.perf_counter() - t
+        mp = {"time_s": dt, "rounds": m["rounds"], "objective": m["obj"], "support": [int(j) for j in m["support"]],
+              "scan_gbs_alg": m["rounds"] * 8.0 * inst.n * inst.p / dt / 1e9,
+              "note": "one HBM pass over X (8np bytes) per round + O(|S|n) backward work; host reads one flag per round"}
     prob.close()
     del prob
     micro = None
@@ -431,6 +441,8 @@ def main():
             line["certified_solves"] = certified
         if micro is not None:
             line["bound_microbench"] = micro
+        if mp is not None:
+            line["matching_pursuit"] = mp
         if cpu is not None:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(line), flush=True)

@@ -115,6 +115,22 @@ int l0l2_bound_batch(l0l2_ctx* ctx, int32_t B,
 int l0l2_upper_batch(l0l2_ctx* ctx, int32_t B, const int64_t* supp_off, const int32_t* supp_idx,
                      double* obj, double* beta_s, void* stream);
 
+/*
+ * l0l2_matching_pursuit — the root heuristic of PAPER.md §"Matching Pursuit Algorithm"
+ * (Algorithm 3; outline P:781-783), run on the device against the resident X.
+ * S ← ∅, β ← 0, r ← y; each round: forward step (every j ∉ S scored by
+ * Δ_j = −β_j c_j + ½β_j²D_j + λ0 with c = Xᵀr, D = ‖X_j‖² + 2λ2, β_j = Proj_[−M,M](c_j/D_j);
+ * the argmin joins S if Δ < 0), then backward step (every j ∈ S scored by
+ * Δ_j = β_j c_j + (½‖X_j‖² − λ2)β_j² − λ0 with the updated residual; the argmin leaves S if
+ * Δ < 0); stop when a round changes nothing or after max_rounds (≤ 0 → 4p + 10).  Argmin ties
+ * → lowest column index (R15).
+ * HOST outputs: beta double[p] (zero off S), support int32[p capacity] ascending, *support_len,
+ * *obj = ½‖y − Xβ‖² + λ2‖β‖² + λ0|S| (a feasible objective of eq:perspective), *rounds (may be NULL).
+ * Errors: L0L2_EINVAL on NULL outputs, L0L2_ECUDA / L0L2_ENOMEM on device failures.
+ */
+int l0l2_matching_pursuit(l0l2_ctx* ctx, int32_t max_rounds, double* beta, int32_t* support, int32_t* support_len,
+                          double* obj, int32_t* rounds);
+
 /* Options of the branch-and-bound driver (Algorithm 1). */
 typedef struct {
   double  gap_tol;          /* stop when (UB − LB)/UB ≤ gap_tol; default 1e-2   */
@@ -125,6 +141,8 @@ typedef struct {
   int64_t warm_bytes_cap;   /* device bytes for parent warm states; 0 → 25% of free HBM          */
   int32_t verbose;          /* 1: one progress line per round on stderr                          */
   int32_t record;           /* 1: keep a per-node trace of this rank (l0l2_solve_trace)           */
+  int32_t init_mp;          /* 1: initial incumbent from l0l2_matching_pursuit, refit on its support by
+                               the upper-bound routine; 0 (default): β = 0            */
 } l0l2_solve_opts;
 
 void l0l2_default_solve_opts(l0l2_solve_opts* o);

@@ -29,7 +29,7 @@ class _Opts(C.Structure):
 class _SolveOpts(C.Structure):
     _fields_ = [("gap_tol", C.c_double), ("time_limit_s", C.c_double), ("node_limit", C.c_int64),
                 ("batch", C.c_int32), ("rebalance_every", C.c_int32), ("warm_bytes_cap", C.c_int64),
-                ("verbose", C.c_int32), ("record", C.c_int32)]
+                ("verbose", C.c_int32), ("record", C.c_int32), ("init_mp", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -71,6 +71,9 @@ def load_library():
     lib.l0l2_bound_batch.restype = C.c_int
     lib.l0l2_upper_batch.argtypes = [P, C.c_int32, P, P, P, P, P]
     lib.l0l2_upper_batch.restype = C.c_int
+    lib.l0l2_matching_pursuit.argtypes = [P, C.c_int32, P, P, C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                          C.POINTER(C.c_int32)]
+    lib.l0l2_matching_pursuit.restype = C.c_int
     lib.l0l2_default_solve_opts.argtypes = [C.POINTER(_SolveOpts)]
     lib.l0l2_default_solve_opts.restype = None
     lib.l0l2_solve.argtypes = [P, C.POINTER(_SolveOpts), P, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -270,6 +273,17 @@ class Problem:
         return obj, betas
 
     # -------------------------------------------------------------- solve / multi-GPU
+    def l0l2_matching_pursuit(self, max_rounds=0):
+        """Algorithm 3 on the device → dict(support, beta, obj, rounds)."""
+        beta = np.zeros(self.p, dtype=np.float64)
+        supp = np.zeros(max(1, self.p), dtype=np.int32)
+        slen, rounds = C.c_int32(), C.c_int32()
+        obj = C.c_double()
+        rc = self._lib.l0l2_matching_pursuit(self._ctx, int(max_rounds), beta.ctypes.data, supp.ctypes.data,
+                                             C.byref(slen), C.byref(obj), C.byref(rounds))
+        _check(rc, self._ctx)
+        return dict(support=supp[:slen.value].copy(), beta=beta, obj=obj.value, rounds=rounds.value)
+
     def l0l2_comm_init(self, nranks, rank, uid: bytes):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         _check(self._lib.l0l2_comm_init(self._ctx, int(nranks), int(rank), C.cast(buf, P)), self._ctx)
@@ -284,13 +298,14 @@ class Problem:
         self.l0l2_comm_init(dist.get_world_size(), dist.get_rank(), obj[0])
 
     def l0l2_solve(self, gap_tol=1e-2, batch=16, time_limit_s=0.0, node_limit=0, rebalance_every=8,
-                   warm_bytes_cap=0, verbose=False, record=False):
+                   warm_bytes_cap=0, verbose=False, record=False, init_mp=False):
         so = _SolveOpts()
         self._lib.l0l2_default_solve_opts(C.byref(so))
         so.gap_tol, so.batch, so.time_limit_s = float(gap_tol), int(batch), float(time_limit_s)
         so.node_limit, so.rebalance_every, so.warm_bytes_cap = int(node_limit), int(rebalance_every), int(warm_bytes_cap)
         so.verbose = int(bool(verbose))
         so.record = int(bool(record))
+        so.init_mp = int(bool(init_mp))
         beta = np.zeros(self.p, dtype=np.float64)
         obj, gap = C.c_double(), C.c_double()
         st = _Stats()

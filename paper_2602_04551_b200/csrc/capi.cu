@@ -3,6 +3,8 @@
 #include <cstdarg>
 #include <cstring>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace l0l2 {
@@ -266,6 +268,24 @@ int l0l2_upper_batch(l0l2_ctx* ctx, int32_t B, const int64_t* supp_off, const in
   int rc = upper_batch(c, B, supp_off, supp_idx, obj, beta_s, (cudaStream_t)stream);
   if (rc) return rc;
   L0L2_CUDA(c, cudaStreamSynchronize((cudaStream_t)stream));
+  return L0L2_OK;
+}
+
+int l0l2_matching_pursuit(l0l2_ctx* ctx, int32_t max_rounds, double* beta, int32_t* support, int32_t* support_len,
+                          double* obj, int32_t* rounds) {
+  if (!ctx) return L0L2_EINVAL;
+  Ctx* c = &ctx->impl;
+  if (!beta || !support || !support_len || !obj) return set_err(c, L0L2_EINVAL, "bad arguments");
+  L0L2_CUDA(c, cudaSetDevice(c->device));
+  std::vector<int32_t> S;
+  std::vector<double> b;
+  int r = 0;
+  int rc = mp_run(c, max_rounds, nullptr, S, b, obj, &r);
+  if (rc) return rc;
+  std::memcpy(beta, b.data(), sizeof(double) * c->p);
+  if (!S.empty()) std::memcpy(support, S.data(), sizeof(int32_t) * S.size());
+  *support_len = (int32_t)S.size();
+  if (rounds) *rounds = r;
   return L0L2_OK;
 }
 

@@ -51,6 +51,13 @@ struct Ctx {
   int *seg_cnt = nullptr;
   int seg_cap = 0, nz_cap = 0;
 
+  // matching-pursuit root heuristic work space (mp.cu, allocated on first use)
+  double *mp_r = nullptr, *mp_beta = nullptr, *mp_log = nullptr;
+  uint8_t* mp_inS = nullptr;
+  int32_t* mp_S = nullptr;
+  void* mp_cand = nullptr;
+  int* mp_state = nullptr;
+
   double *node_f = nullptr;                                 // per-node scalars (admm.cu)
   int *node_i = nullptr;
   int *badflag = nullptr;
@@ -138,6 +145,10 @@ int unpack_warm(Ctx* c, int nb, double* const* warm_ptrs_dev, cudaStream_t st);
 int dual_residual(Ctx* c, int nb, double* dual_r, int64_t ldr, cudaStream_t st);
 int upper_batch(Ctx* c, int B, const int64_t* supp_off, const int32_t* supp_idx, double* obj,
                 double* beta_s, cudaStream_t st);
+
+// Algorithm 3 (matching pursuit) on the device; S_out ascending, beta_out length p.
+int mp_run(Ctx* c, int max_rounds, cudaStream_t st, std::vector<int32_t>& S_out, std::vector<double>& beta_out,
+           double* obj, int* rounds);
 
 void comm_free(Ctx* c);
 

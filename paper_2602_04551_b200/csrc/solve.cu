@@ -546,6 +546,7 @@ void l0l2_default_solve_opts(l0l2_solve_opts* o) {
   o->warm_bytes_cap = 0;
   o->verbose = 0;
   o->record = 0;
+  o->init_mp = 0;
 }
 
 int l0l2_nccl_unique_id(uint8_t out[128]) {
@@ -629,6 +630,39 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
   int rc = S.alloc_bufs(o.batch);
   if (rc) return rc;
   S.UB = 0.5 * c->yy;   // β = 0 is feasible
+  if (o.init_mp) {
+    // root heuristic (Algorithm 3): MP's own point, then the box ridge on its support
+    auto t0 = Clock::now();
+    std::vector<int32_t> mS;
+    std::vector<double> mb;
+    double mobj = 0.0;
+    if ((rc = mp_run(c, 0, S.st, mS, mb, &mobj, nullptr))) return rc;
+    if (mobj < S.UB) {
+      S.UB = mobj;
+      S.inc_S = mS;
+      S.inc_b.assign(mS.size(), 0.0);
+      for (size_t i = 0; i < mS.size(); i++) S.inc_b[i] = mb[mS[i]];
+    }
+    if (!mS.empty()) {
+      const int64_t off[2] = {0, (int64_t)mS.size()};
+      int64_t* doff = (int64_t*)c->scratch_n(4, sizeof(int64_t) * 2 + sizeof(int32_t) * mS.size());
+      double* dres = (double*)c->scratch_n(5, sizeof(double) * (mS.size() + 1));
+      if (!doff || !dres) return set_err(c, L0L2_ENOMEM, "mp refit buffers");
+      int32_t* didx = (int32_t*)(doff + 2);
+      L0L2_CUDA(c, cudaMemcpyAsync(doff, off, sizeof(off), cudaMemcpyHostToDevice, S.st));
+      L0L2_CUDA(c, cudaMemcpyAsync(didx, mS.data(), sizeof(int32_t) * mS.size(), cudaMemcpyHostToDevice, S.st));
+      if ((rc = upper_batch(c, 1, doff, didx, dres, dres + 1, S.st))) return rc;
+      std::vector<double> h(mS.size() + 1);
+      L0L2_CUDA(c, cudaMemcpyAsync(h.data(), dres, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, S.st));
+      L0L2_CUDA(c, cudaStreamSynchronize(S.st));
+      if (h[0] < S.UB) {
+        S.UB = h[0];
+        S.inc_S = mS;
+        S.inc_b.assign(h.begin() + 1, h.end());
+      }
+    }
+    S.t_upper += secs(t0);
+  }
   S.open.push(Node{-INFINITY, 0, 0, {}, {}, -1});
   double LB = -INFINITY;
   int status = 0;

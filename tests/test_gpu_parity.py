@@ -301,3 +301,49 @@ def test_c4_full_size_sampled():
     assert res["stats"]["nodes"] == golden["nodes"]
     assert abs(res["obj"] - golden["ub"]) <= 1e-6 * golden["ub"]
     prob.close()
+
+
+# ---------------------------------------------------------------- matching pursuit (Algorithm 3)
+def test_matching_pursuit_parity(case):
+    """l0l2_matching_pursuit vs the oracle's Algorithm 3: same support (bit-exact
+    integer decisions), β within 1e-9, objective within 1e-9 relative, same number of rounds."""
+    name, inst, lam0, lam2, M, P = case
+    prob = Problem(inst.X, inst.y, lam0, lam2, M, rho=P.rho)
+    g = prob.l0l2_matching_pursuit()
+    r = O.matching_pursuit(P)
+    assert list(g["support"]) == list(r.support), name
+    assert rel(g["beta"], r.beta) < 1e-9
+    assert abs(g["obj"] - r.obj) <= 1e-9 * abs(r.obj)
+    assert g["rounds"] == r.rounds
+    assert np.all(np.abs(g["beta"]) <= M)
+    prob.close()
+
+
+def test_matching_pursuit_c4_full_size():
+    """Algorithm 3 at the bench's full size (C4: n=1000, p=1e5) vs the oracle."""
+    inst = synth.config_instance("C4", seed=0)
+    P = O.Problem(inst.X, inst.y, inst.lambda0, inst.lambda2, inst.M, rho=1.0)
+    prob = Problem(inst.X, inst.y, inst.lambda0, inst.lambda2, inst.M, rho=1.0)
+    g = prob.l0l2_matching_pursuit()
+    r = O.matching_pursuit(P)
+    assert list(g["support"]) == list(r.support)
+    assert rel(g["beta"], r.beta) < 1e-9
+    assert abs(g["obj"] - r.obj) <= 1e-9 * abs(r.obj)
+    assert g["rounds"] == r.rounds
+    prob.close()
+
+
+@pytest.mark.parametrize("seed", [0, 3])
+def test_solve_with_mp_incumbent(seed):
+    """l0l2_solve with the matching-pursuit incumbent (init_mp) still certifies the
+    brute-force optimum, and its answer is never worse than the heuristic's own objective."""
+    inst = synth.config_instance("C1", seed=seed)
+    P = O.Problem(inst.X, inst.y, inst.lambda0, inst.lambda2, inst.M)
+    bf_obj, bf_S, _ = O.brute_force(P)
+    prob = Problem(inst.X, inst.y, inst.lambda0, inst.lambda2, inst.M, rho=P.rho, node_tol=1e-10, max_iters=20000)
+    mp = prob.l0l2_matching_pursuit()
+    res = prob.l0l2_solve(gap_tol=1e-9, batch=8, init_mp=True)
+    assert abs(res["obj"] - bf_obj) <= 1e-9 * abs(bf_obj)
+    assert list(res["support"]) == list(bf_S)
+    assert res["obj"] <= mp["obj"] * (1 + 1e-12)
+    prob.close()
