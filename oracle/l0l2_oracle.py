@@ -221,10 +221,11 @@ class NodeResult:
     branch_j: int
     kkt: float
     duals: list = field(default_factory=list)   # (iteration, dual) of every check
+    pruned: bool = False    # stopped early: LB_best ≥ prune_ub at a check (early prune, R16)
 
 
 def admm_node(P: Problem, code, warm=None, parent_lb=-math.inf, node_tol=1e-4,
-              check_every=10, max_iters=10000, int_tol=1e-4) -> NodeResult:
+              check_every=10, max_iters=10000, int_tol=1e-4, prune_ub=math.inf) -> NodeResult:
     """ADMM on eq:ADMM1 for one node, warm start P:543.
 
     Start: (β, v) = parent state or zeros; β_i ← 0 on F0; refresh b = D(c + ρβ − v),
@@ -237,6 +238,8 @@ def admm_node(P: Problem, code, warm=None, parent_lb=-math.inf, node_tol=1e-4,
     Finalize (S:197, S:224, S:253, S:381): LB = max(LB_best, parent LB); ẑ from β;
     integral if every free ẑ is within int_tol of {0,1}; support = F1 ∪ {free: ẑ ≥ ½};
     branch j = argmax_free min(ẑ, 1−ẑ), ties → larger |β_j|, then lower index [R10].
+    Early prune [R16, SURVEY §8(f) rank 2]: a check that does not converge but finds
+    LB_best ≥ prune_ub stops the node (it will be pruned; any dual is a valid bound).
     """
     code = np.asarray(code, dtype=np.int8)
     p, rho = P.p, P.rho
@@ -254,6 +257,7 @@ def admm_node(P: Problem, code, warm=None, parent_lb=-math.inf, node_tol=1e-4,
     duals = []
     it = 0
     converged = False
+    pruned = False
     beta_prev = beta.copy()
     while it < max_iters:
         it += 1
@@ -271,6 +275,9 @@ def admm_node(P: Problem, code, warm=None, parent_lb=-math.inf, node_tol=1e-4,
             if (primal - lb_best) / max(1.0, abs(primal)) <= node_tol:
                 converged = True
                 break
+            if lb_best >= prune_ub:
+                pruned = True
+                break
     kkt = max(float(np.max(np.abs(b - beta), initial=0.0)),
               rho * float(np.max(np.abs(beta - beta_prev), initial=0.0))) / (1.0 + float(np.max(np.abs(P.c), initial=0.0)))
     z = recover_z(beta, code, P.lam0, P.lam2, P.M)
@@ -286,7 +293,7 @@ def admm_node(P: Problem, code, warm=None, parent_lb=-math.inf, node_tol=1e-4,
         branch_j = int(cand[order[0]])
     return NodeResult(lb=max(lb_best, parent_lb), lb_best=lb_best, primal=primal, beta=beta, v=v, b=b,
                       iters=it, converged=converged, z=z, integral=integral, support=support,
-                      branch_j=branch_j, kkt=kkt, duals=duals)
+                      branch_j=branch_j, kkt=kkt, duals=duals, pruned=pruned)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -428,7 +435,8 @@ def relaxation_fista(P: Problem, code, tol=1e-12, max_iters=200000):
 # ----------------------------------------------------------------------------------------------
 
 def bnb_solve(P: Problem, B=1, gap_tol=1e-2, node_tol=1e-4, check_every=10, max_iters=10000,
-              int_tol=1e-4, prune_tol=1e-12, node_limit=None, time_limit=None, record=False):
+              int_tol=1e-4, prune_tol=1e-12, node_limit=None, time_limit=None, record=False,
+              early_prune=False):
     """Best-first synchronous-round BnB (Algorithm 1) [R9, R11].
 
     UB starts at ½‖y‖² (β = 0 is feasible).  Each round: drop open nodes with
@@ -438,6 +446,9 @@ def bnb_solve(P: Problem, B=1, gap_tol=1e-2, node_tol=1e-4, check_every=10, max_
     of the round's UB improvements (lowest id wins ties); then in id order prune by
     LB_u ≥ UB(1−prune_tol) or integral ẑ, else branch on j into
     (F0∪{j}, F1) then (F0, F1∪{j}) with LB_u and the parent's (β, v).
+    early_prune [R16]: each node's ADMM stops at the first check whose LB_best ≥ UB(1−prune_tol)
+    with UB the incumbent at the start of the round (the node is then pruned by the rule above,
+    since the round can only lower UB).
     """
     t0 = time.perf_counter()
     p = P.p
@@ -469,10 +480,12 @@ def bnb_solve(P: Problem, B=1, gap_tol=1e-2, node_tol=1e-4, check_every=10, max_
         batch, open_nodes = open_nodes[:B], open_nodes[B:]
         rounds += 1
         results = []
+        prune_ub = UB * (1 - prune_tol) if early_prune else math.inf
         for (plb, uid, depth, F0, F1, warm) in batch:
             code = make_code(p, F0, F1)
             res = admm_node(P, code, warm=warm, parent_lb=plb, node_tol=node_tol,
-                            check_every=check_every, max_iters=max_iters, int_tol=int_tol)
+                            check_every=check_every, max_iters=max_iters, int_tol=int_tol,
+                            prune_ub=prune_ub)
             obj, bS = upper_bound(P, res.support)
             results.append((uid, depth, F0, F1, res, obj, bS))
             nodes += 1
@@ -486,7 +499,7 @@ def bnb_solve(P: Problem, B=1, gap_tol=1e-2, node_tol=1e-4, check_every=10, max_
                 trace.append(dict(id=uid, depth=depth, F0=F0, F1=F1, lb=res.lb, lb_best=res.lb_best,
                                   primal=res.primal, iters=res.iters, branch_j=res.branch_j,
                                   integral=res.integral, support=tuple(res.support.tolist()), ub=obj,
-                                  pruned=pruned, round=rounds))
+                                  pruned=pruned, early=res.pruned, round=rounds))
             if pruned:
                 continue
             j = res.branch_j

@@ -507,3 +507,22 @@ def test_mp_descent_fixed_point_and_valid_upper_bound(seed):
     if len(mp.support):
         assert np.min(O.mp_backward_scores(P, r, mp.beta, mp.support)) >= 0
     assert mp.obj >= O.brute_force(P)[0] - 1e-9
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_early_prune_keeps_the_certificate(seed):
+    """Early prune (R16) changes only how long pruned nodes run: the BnB
+    still certifies the brute-force optimum, solves no more node iterations, and every node that
+    stopped early is pruned (its LB ≥ the incumbent)."""
+    inst = synth.make_instance(40, 14, 3, 0.3, 4.0, 20 + seed)
+    lam2 = max(synth.tune_lambda2(inst), 0.05)
+    P = O.Problem(inst.X, inst.y, synth.lambda0_rule(inst, lam2), lam2, synth.bigM_rule(inst, lam2))
+    bf_obj, bf_S, _ = O.brute_force(P)
+    a = O.bnb_solve(P, B=4, gap_tol=1e-9, node_tol=1e-9, record=True)
+    b = O.bnb_solve(P, B=4, gap_tol=1e-9, node_tol=1e-9, record=True, early_prune=True)
+    for r in (a, b):
+        assert r["obj"] == pytest.approx(bf_obj, rel=1e-9)
+        assert list(r["support"]) == list(bf_S)
+    early = [t for t in b["trace"] if t["early"]]
+    assert all(t["pruned"] for t in early)          # an early-stopped node is always pruned
+    assert not any(t["early"] for t in a["trace"])
