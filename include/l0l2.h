@@ -37,6 +37,7 @@ extern "C" {
 #define L0L2_FLAG_CONVERGED 1u  /* relative primal-dual gap ≤ node_tol at a check */
 #define L0L2_FLAG_INTEGRAL  2u  /* every free ẑ within int_tol of {0,1} (P:258 prune (i)) */
 #define L0L2_FLAG_MAXITER   4u  /* stopped at max_iters */
+#define L0L2_FLAG_PRUNED    8u  /* stopped early: best dual ≥ the prune threshold (l0l2_solve early_prune) */
 
 typedef struct l0l2_ctx l0l2_ctx;
 
@@ -143,6 +144,9 @@ typedef struct {
   int32_t record;           /* 1: keep a per-node trace of this rank (l0l2_solve_trace)           */
   int32_t init_mp;          /* 1: initial incumbent from l0l2_matching_pursuit, refit on its support by
                                the upper-bound routine; 0 (default): β = 0            */
+  int32_t early_prune;      /* 1: a node's ADMM stops at the first check whose best dual ≥ UB(1−1e-12),
+                               UB = the incumbent at the start of its round (the node is pruned
+                               anyway; R16); 0 (default): run to node_tol        */
 } l0l2_solve_opts;
 
 void l0l2_default_solve_opts(l0l2_solve_opts* o);

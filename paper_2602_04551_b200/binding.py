@@ -11,7 +11,7 @@ _LIB_PATH = os.path.join(HERE, os.environ.get("L0L2_LIB", "libl0l2.so"))   # L0L
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL = 0, -1, -2, -3, -4
 WNOTCONV, WLIMIT = 1, 2
-FLAG_CONVERGED, FLAG_INTEGRAL, FLAG_MAXITER = 1, 2, 4
+FLAG_CONVERGED, FLAG_INTEGRAL, FLAG_MAXITER, FLAG_PRUNED = 1, 2, 4, 8
 
 
 class L0L2Error(RuntimeError):
@@ -29,7 +29,8 @@ class _Opts(C.Structure):
 class _SolveOpts(C.Structure):
     _fields_ = [("gap_tol", C.c_double), ("time_limit_s", C.c_double), ("node_limit", C.c_int64),
                 ("batch", C.c_int32), ("rebalance_every", C.c_int32), ("warm_bytes_cap", C.c_int64),
-                ("verbose", C.c_int32), ("record", C.c_int32), ("init_mp", C.c_int32)]
+                ("verbose", C.c_int32), ("record", C.c_int32), ("init_mp", C.c_int32),
+                ("early_prune", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -298,7 +299,7 @@ class Problem:
         self.l0l2_comm_init(dist.get_world_size(), dist.get_rank(), obj[0])
 
     def l0l2_solve(self, gap_tol=1e-2, batch=16, time_limit_s=0.0, node_limit=0, rebalance_every=8,
-                   warm_bytes_cap=0, verbose=False, record=False, init_mp=False):
+                   warm_bytes_cap=0, verbose=False, record=False, init_mp=False, early_prune=False):
         so = _SolveOpts()
         self._lib.l0l2_default_solve_opts(C.byref(so))
         so.gap_tol, so.batch, so.time_limit_s = float(gap_tol), int(batch), float(time_limit_s)
@@ -306,6 +307,7 @@ class Problem:
         so.verbose = int(bool(verbose))
         so.record = int(bool(record))
         so.init_mp = int(bool(init_mp))
+        so.early_prune = int(bool(early_prune))
         beta = np.zeros(self.p, dtype=np.float64)
         obj, gap = C.c_double(), C.c_double()
         st = _Stats()

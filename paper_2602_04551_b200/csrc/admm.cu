@@ -43,7 +43,7 @@ constexpr int NW = kAdmmThreads / 32;   // 16 warps: 14 MMA + 2 epilogue
 constexpr int NEW = 2;                  // epilogue warps
 constexpr int NH = kBC / 8;             // node halves (one per CTA of a pair)
 static_assert(NH == 2, "a CTA pair serves the two node halves");
-constexpr int F_ACTIVE = 8;             // internal node flag bit (not exported)
+constexpr int F_ACTIVE = 64;            // internal node flag bit (not exported)
 
 struct KP {
   const double* __restrict__ Z;
@@ -64,6 +64,7 @@ struct KP {
   int64_t ld, n, n8, p8;
   int ntiles, nsr, nb, check_every, max_iters, pfd;   // nsr: tile sub-ranges (= grid)
   unsigned act_mask;               // node slots run by this launch (outputs written for these only)
+  double prune_ub;                 // early prune threshold (R16; +inf = off)
   int pfs;                         // tiles L2-prefetched by prefill (during the grid reduction)
   int tsplit;                      // bulk copies per Z tile (divides kPt)
   double rho, inv_rho, lam0, lam2, M, yy, node_tol;
@@ -289,7 +290,9 @@ __device__ void issue_stage_m(const KP& k, Smem& s, int m, int t0, int t1) {
   const int tile = m < t1 - t0 ? t0 + m : -1;
   s.stile[sg] = tile;
   if (tile >= 0) {
+#ifndef L0L2_NOFENCE
     fence_proxy_async_smem();
+#endif
     issue_stage(k, s, tile, sg);
     if (k.pfd > 0 && tile + k.pfd < t1) prefetch_l2(k.Z + (int64_t)(tile + k.pfd) * kPt * k.ld, tile_bytes(k));
   } else {
@@ -308,6 +311,7 @@ __device__ void issue_stage_m(const KP& k, Smem& s, int m, int t0, int t1) {
 // changes, those rows may have been written by the partner CTA, which may still be sweeping: the
 // issue is deferred (sched[8]) to the start of the next sweep, which follows a grid barrier.
 __device__ void issue_first(const KP& k, Smem& s) {
+  fence_proxy_async_smem();   // the launch's generic zeroing of the ring precedes its first TMA writes
   for (int m = 0; m < NST; m++) issue_stage_m(k, s, m, s.sched[6], s.sched[7]);
   // the grid reduction that follows leaves HBM idle: pull the sweep's next tiles into L2 meanwhile
   const int t0 = s.sched[6], t1 = s.sched[7];
@@ -417,7 +421,9 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       const double* T = s.tiles + (size_t)(m % NST) * kPt * ld + cA * ld + kA;
       double sc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
+#ifndef EXP_NOADJ
       for (int i = 0; i < KS; i++) dmma(sc[i & 3], T[4 * (warp + NMW * i)], uf[i]);
+#endif
       double* sp = s.spart + (m & 1) * NMW * 64 + warp * 64;
       // C fragment: row (col j) = lane>>2, cols (node) = 2*(lane&3) + {0,1}
       sp[cA * 8 + 2 * kA] = (sc[0][0] + sc[1][0]) + (sc[2][0] + sc[3][0]);
@@ -442,12 +448,14 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       // ---- forward: U⁺(rows × 8 nodes) += Z_J (rows × 8 cols) · W_J (8 cols × 8 nodes)
       const double b0 = W[cA * 12 + kA];         // B[k = j][n = node]
       const double b1 = W[cA * 12 + 4 + kA];
+      // two passes (k = cols 0-3, then 4-7), so consecutive DMMAs never share an accumulator (the
+      // asm volatile DMMAs issue in source order; back-to-back dependent pairs stalled on latency)
+#ifndef EXP_NOFWD
 #pragma unroll
-      for (int i = 0; i < MT; i++) {
-        const int row = 8 * (warp + NMW * i);
-        dmma(acc[i], T[row], b0);                // A[m = row][k = col j]
-        dmma(acc[i], T[4 * ld + row], b1);
-      }
+      for (int i = 0; i < MT; i++) dmma(acc[i], T[8 * (warp + NMW * i)], b0);            // A[m = row][k = col j]
+#pragma unroll
+      for (int i = 0; i < MT; i++) dmma(acc[i], T[4 * ld + 8 * (warp + NMW * i)], b1);
+#endif
       PROF_ACC(3);
       if (!fused) mbar_arrive_warp(&s.sready[m & 1]);   // w⁺ buffer m&1 free again
       // release stage m: the last MMA warp to finish its forward refills the slot with stage m + NST
@@ -515,6 +523,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
         hph ^= 1u << (m & 1);
       }
       PROF_ACC(2);
+#ifndef EXP_NOEPI
       if (fused) {
         // S_J = Σ over the NMW k-split partials, pairwise in a fixed tree (short dependency chain)
         const double* sp = s.spart + (m & 1) * NMW * 64 + j * 8 + nd;
@@ -557,6 +566,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
           seg_n += __popc(mnode);
         }
       }
+#endif
       s.Ws[(m & 1) * 8 * 12 + nd * 12 + j] = wn;
       mbar_arrive_warp(&s.wready[m & 1]);
       PROF_ACC(5);
@@ -848,6 +858,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
         s.red[nd] = lbb;
         bool conv = (primal - lbb) / fmax(1.0, fabs(primal)) <= k.node_tol;
         if (conv) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_CONVERGED;
+        else if (lbb >= k.prune_ub) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_PRUNED;   // early prune (R16)
         else if (it == k.max_iters) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_MAXITER;
         s.flags[nd] = fl;
         if (blockIdx.x == 0) {
@@ -877,7 +888,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     k.out_lb[nd] = fmax(lbb, plb);
     k.out_primal[nd] = k.nodef[nd * 4 + 1];
     k.out_iters[nd] = k.nodei[nd * 2 + 1];
-    k.out_flags[nd] = (uint8_t)(s.flags[nd] & (L0L2_FLAG_CONVERGED | L0L2_FLAG_MAXITER));
+    k.out_flags[nd] = (uint8_t)(s.flags[nd] & (L0L2_FLAG_CONVERGED | L0L2_FLAG_MAXITER | L0L2_FLAG_PRUNED));
   }
 }
 
@@ -1160,6 +1171,7 @@ int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
   L0L2_LAUNCHED(c);
   KP k{};
   k.act_mask = mask;
+  k.prune_ub = a.prune_ub;
   k.Z = c->Z; k.Lt = c->Lt;
   k.stt = c->stt; k.bchk = c->bchk;
   k.U = c->U; k.Ub = c->Ub; k.Upart = c->Upart; k.sums = c->sums; k.sums2 = c->sums2;

@@ -134,6 +134,7 @@ struct BoundArgs {
   double *lb, *primal;          // device [nb]
   int *iters;                   // device [nb]
   uint8_t* flags;               // device [nb]
+  double prune_ub = INFINITY;   // stop a node once its best dual reaches this (early prune, R16)
 };
 int pack_group(Ctx* c, int nb, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
                const double* const* warm_ptrs_dev, cudaStream_t st);

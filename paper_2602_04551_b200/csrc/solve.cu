@@ -279,6 +279,7 @@ struct Solver {
       int rc = pack_group(c, nb, d.fix_off + g0, dfi, dfv, (const double* const*)d.wptr, st);
       if (rc) return rc;
       BoundArgs a{nb, d.parent_lb + g0, d.lb + g0, d.primal + g0, d.iters + g0, d.flags + g0};
+      if (o.early_prune) a.prune_ub = UB * (1.0 - 1e-12);   // UB of the round's start (R16)
       if ((rc = run_admm(c, a, st))) return rc;
       if ((rc = finalize_group(c, nb, nullptr, d.branch + g0, d.flags + g0, d.scnt + g0, d.sidx, p, st))) return rc;
       if ((rc = unpack_warm(c, nb, d.wptr + kBC, st))) return rc;
@@ -547,6 +548,7 @@ void l0l2_default_solve_opts(l0l2_solve_opts* o) {
   o->verbose = 0;
   o->record = 0;
   o->init_mp = 0;
+  o->early_prune = 0;
 }
 
 int l0l2_nccl_unique_id(uint8_t out[128]) {

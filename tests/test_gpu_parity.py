@@ -22,7 +22,7 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from paper_2602_04551_b200 import FLAG_CONVERGED, FLAG_INTEGRAL, L0L2Error, Problem  # noqa: E402
+from paper_2602_04551_b200 import FLAG_CONVERGED, FLAG_INTEGRAL, FLAG_PRUNED, L0L2Error, Problem  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -269,6 +269,33 @@ def test_solve_tree_parity(B):
         assert g["branch_j"] == t["branch_j"] or t["branch_j"] < 0
         matched += 1
     assert matched == len(res["trace"]) == ref["nodes"]
+    prob.close()
+
+
+@pytest.mark.parametrize("B", [1, 16])
+def test_solve_tree_parity_early_prune(B):
+    """Early prune (R16) on both sides: node-for-node parity with the oracle's BnB (same ids,
+    bounds, iterations, branches, and the same nodes stopped early), same certificate."""
+    inst = synth.make_instance(80, 60, 5, 0.3, 3.0, 21)
+    lam2 = 0.5
+    lam0 = synth.lambda0_rule(inst, lam2)
+    M = synth.bigM_rule(inst, lam2)
+    P = O.Problem(inst.X, inst.y, lam0, lam2, M)
+    ref = O.bnb_solve(P, B=B, gap_tol=1e-4, node_tol=1e-8, record=True, early_prune=True)
+    assert any(t["early"] for t in ref["trace"])
+    prob = Problem(inst.X, inst.y, lam0, lam2, M, rho=P.rho, node_tol=1e-8)
+    res = prob.l0l2_solve(gap_tol=1e-4, batch=B, record=True, early_prune=True)
+    assert abs(res["obj"] - ref["obj"]) <= 1e-9 * abs(ref["obj"])
+    assert np.array_equal(res["support"], ref["support"])
+    gt = {t["id"]: t for t in res["trace"]}
+    for t in ref["trace"]:
+        g = gt.get(t["id"])
+        assert g is not None, ("node missing on GPU", t["id"])
+        assert abs(g["lb"] - t["lb"]) <= 1e-6 * max(1.0, abs(t["lb"]))
+        assert g["iters"] == t["iters"]
+        assert bool(g["flags"] & FLAG_PRUNED) == t["early"]
+        assert g["branch_j"] == t["branch_j"] or t["branch_j"] < 0
+    assert len(res["trace"]) == ref["nodes"]
     prob.close()
 
 
