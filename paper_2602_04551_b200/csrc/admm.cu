@@ -65,6 +65,7 @@ struct KP {
   int ntiles, nsr, nb, check_every, max_iters, pfd;   // nsr: tile sub-ranges (= grid)
   unsigned act_mask;               // node slots run by this launch (outputs written for these only)
   double prune_ub;                 // early prune threshold (R16; +inf = off)
+  int compact;                     // node-slot compaction allowed (tuning / test hook)
   int pfs;                         // tiles L2-prefetched by prefill (during the grid reduction)
   int tsplit;                      // bulk copies per Z tile (divides kPt)
   double rho, inv_rho, lam0, lam2, M, yy, node_tol;
@@ -318,7 +319,10 @@ __device__ void issue_first(const KP& k, Smem& s) {
   for (int t = t0 + NST + k.pfd; t < t1 && t < t0 + NST + k.pfs; t++) prefetch_l2(k.Z + (int64_t)t * kPt * k.ld, tile_bytes(k));
 }
 
-__device__ void prefill(const KP& k, Smem& s, int sw) {
+// The CTA's node half and tile range of a sweep, from the current node flags (every CTA decides
+// from the same flags).  Paired: both halves active → CTA g serves half g&1 on sub-ranges
+// 2⌊g/2⌋, 2⌊g/2⌋+1.  Otherwise CTA g serves the active half on sub-range g.
+__device__ void choose_mode(const KP& k, Smem& s) {
   const int g = blockIdx.x;
   int a0 = 0, a1 = 0;
   for (int nd = 0; nd < 8; nd++) {
@@ -326,17 +330,28 @@ __device__ void prefill(const KP& k, Smem& s, int sw) {
     a1 |= s.flags[8 + nd] & F_ACTIVE;
   }
   const bool paired = a0 && a1;
-  const int half = paired ? (g & 1) : (a0 ? 0 : 1);
-  const bool changed = sw > 0 && (half != s.sched[4] || (int)paired != s.sched[5]);
-  s.sched[4] = half;
+  s.sched[4] = paired ? (g & 1) : (a0 ? 0 : 1);
   s.sched[5] = paired;
   s.sched[6] = paired ? sub_t(k, g & ~1) : sub_t(k, g);
   s.sched[7] = paired ? sub_t(k, (g & ~1) + 2) : sub_t(k, g + 1);
+}
+
+// Start sweep number `sw` (thread 0, after the CTA barrier that ends the previous sweep): issue its
+// first NST stages now, so they stream in while the grid reduces u — unless a check decision
+// (which may retire nodes, change the mode and permute node slots) comes before that sweep
+// (defer): then mode and first stages are settled at the start of the sweep (deferred_start),
+// after the grid barrier.  The CTA's next tiles hold β, v rows that it wrote itself (epilogue:
+// generic → async proxy fence before the CTA barrier) while the mode stays; any other case
+// crosses a grid barrier first.
+__device__ void prefill(const KP& k, Smem& s, int sw, bool defer) {
   s.sched[0] = sw;
+  s.sched[8] = defer;
   // stages issued now and not yet consumed (waited for by the drain at the end of the launch)
-  s.sched[1] = changed ? 0 : min(NST, s.sched[7] - s.sched[6] + 1);
-  s.sched[8] = changed;
-  if (!changed) issue_first(k, s);
+  s.sched[1] = 0;
+  if (defer) return;
+  choose_mode(k, s);
+  s.sched[1] = min(NST, s.sched[7] - s.sched[6] + 1);
+  issue_first(k, s);
 }
 
 // One sweep over this CTA's tiles, warp-specialised:
@@ -352,18 +367,21 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
   const int g = blockIdx.x;
   constexpr bool fused = (MODE == SW_FUSED);
   const bool is_mma = warp < NMW;
-  // this sweep's node half and sub-ranges (fixed by prefill; s.sched[4..7] do not change until
-  // the CTA barrier at the end of the sweep)
+  if (s.sched[8]) {   // deferred start (prefill); a grid barrier has passed.  (sched[8] is rewritten
+                      // only by the next prefill, so every thread takes this branch.)
+    if (tid == 0) {
+      choose_mode(k, s);
+      issue_first(k, s);
+    }
+    __syncthreads();   // the mode below, and the scheduler state before the in-sweep issuers
+  }
+  // this sweep's node half and sub-ranges (s.sched[4..7] do not change until the CTA barrier at
+  // the end of the sweep)
   const int h = s.sched[4];
   const bool paired = s.sched[5] != 0;
   const int sr0 = paired ? (g & ~1) : g;
   const int tb = paired ? sub_t(k, sr0 + 1) : 0x7fffffff;   // first tile of the second sub-range
   const int t0s = s.sched[6], t1s = s.sched[7];               // this sweep's tile range
-  if (s.sched[8]) {   // deferred by a mode change (prefill); a grid barrier has passed.  (sched[8]
-                      // is rewritten only by the next prefill, so every thread takes this branch.)
-    if (tid == 0) issue_first(k, s);
-    __syncthreads();   // orders the scheduler state before the in-sweep issuers (acq_rel below)
-  }
   // wait for ring stage m; returns its tile (−1: the CTA's sweep is over)
   auto stage = [&](int m) {
     const int sg = m % NST;
@@ -583,7 +601,8 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
     if (paired && sr == sr0 + 1) eflush();
   }
   __syncthreads();
-  if (tid == 0) prefill(k, s, s.sched[0] + 1);
+  // a check decision follows a check sweep and the dense-primal sweep: defer the next start
+  if (tid == 0) prefill(k, s, s.sched[0] + 1, check || MODE == SW_FWD_BETA);
   // per-sub-range check sums of the CTA's 8 nodes (fixed order over the tile's 8 columns)
   if (fused && check && tid < (paired ? 2 : 1) * 8 * 4) {
     const int si = tid >> 5, nd = (tid >> 2) & 7, q = tid & 3;
@@ -757,6 +776,50 @@ __device__ void lmatvec_partial(const KP& k, Smem& s) {
   }
 }
 
+// Node-slot compaction (paired → single-half mode with all active nodes in half 0): exchange
+// slots a_i ↔ b_i.  Every CTA swaps its per-node shared state; block 0 the per-node scalars in
+// HBM; CTA g the state blocks and b_chk rows of the tiles of sub-range g and rows
+// [n·g/G, n·(g+1)/G) of u.  A node's arithmetic does not depend on its slot, so results are
+// bitwise those without compaction.  Applied again (an involution) before the outputs.
+__device__ void swap_slots(const KP& k, Smem& s, const int* pa, const int* pb, int np) {
+  const int tid = threadIdx.x, g = blockIdx.x, G = gridDim.x;
+  __syncthreads();
+  if (tid == 0)
+    for (int q = 0; q < np; q++) {
+      const int a = pa[q], b = pb[q];
+      int f = s.flags[a]; s.flags[a] = s.flags[b]; s.flags[b] = f;
+      double r = s.red[a]; s.red[a] = s.red[b]; s.red[b] = r;
+      if (g == 0) {
+        for (int i = 0; i < 4; i++) { double t = k.nodef[a * 4 + i]; k.nodef[a * 4 + i] = k.nodef[b * 4 + i]; k.nodef[b * 4 + i] = t; }
+        for (int i = 0; i < 2; i++) { int t = k.nodei[a * 2 + i]; k.nodei[a * 2 + i] = k.nodei[b * 2 + i]; k.nodei[b * 2 + i] = t; }
+      }
+    }
+  const int t0 = sub_t(k, g), t1 = sub_t(k, g + 1);
+  const int64_t cols = (int64_t)(t1 - t0) * kPt;
+  for (int64_t e = tid; e < cols * np; e += blockDim.x) {
+    const int q = (int)(e % np);
+    const int64_t j = (int64_t)t0 * kPt + e / np;
+    const int a = pa[q], b = pb[q];
+    double* B = k.stt + st_beta(j, 0);
+    double t = B[a]; B[a] = B[b]; B[b] = t;
+    t = B[STB + a]; B[STB + a] = B[STB + b]; B[STB + b] = t;
+    uint8_t* C = &st_code(k.stt, j, 0);
+    uint8_t c = C[a]; C[a] = C[b]; C[b] = c;
+    double* H = k.bchk + j * kBC;
+    t = H[a]; H[a] = H[b]; H[b] = t;
+  }
+  const int64_t r0 = k.n8 * g / G, r1 = k.n8 * (g + 1) / G;
+  for (int64_t e = tid; e < (r1 - r0) * np; e += blockDim.x) {
+    const int q = (int)(e % np);
+    const int64_t row = r0 + e / np;
+    double* ua = k.U + (int64_t)pa[q] * k.ld + row;
+    double* ub = k.U + (int64_t)pb[q] * k.ld + row;
+    const double t = *ua; *ua = *ub; *ub = t;
+  }
+  fence_proxy_async_global();   // the next sweep reads the state blocks with TMA
+  grid_sync(k.bar);
+}
+
 template <int KS, int MT>
 __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -797,7 +860,9 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   if (tid < NW * 8) prof_s[tid / 8][tid % 8] = 0;
 #endif
   unsigned phases = 0, hph = 0;
-  if (tid == 0) prefill(k, s, 0);
+  __shared__ int swp_a[8], swp_b[8];   // slot pairs exchanged by the compaction (same in every thread)
+  int nswp = 0;
+  if (tid == 0) prefill(k, s, 0, false);
   __syncthreads();   // the sweep reads its node half and sub-ranges from s.sched
 
   // u0 = Z (c + ρβ0 − v0), then the warm/cold refresh sweep (R6)
@@ -871,10 +936,26 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
       }
     }
     __syncthreads();
-    int any = 0;
-    for (int nd = 0; nd < kBC; nd++) any |= s.flags[nd] & F_ACTIVE;
-    if (!any) break;
+    unsigned am = 0;
+    for (int nd = 0; nd < kBC; nd++) am |= (s.flags[nd] & F_ACTIVE) ? 1u << nd : 0u;
+    if (!am) break;
+    // ≤ 8 active nodes spread over both halves: move them into half 0 (the next sweep then runs
+    // in single-half mode on every SM instead of paired); at most once per launch
+    if (k.compact && nswp == 0 && __popc(am) <= 8 && (am & 0xFFu) && (am & 0xFF00u)) {
+      int np = 0, ib = 0;
+      for (int a = 8; a < 16; a++) {
+        if (!((am >> a) & 1u)) continue;
+        while ((am >> ib) & 1u) ib++;   // next inactive slot of half 0 (exists: |active| ≤ 8)
+        swp_a[np] = a;
+        swp_b[np] = ib++;
+        np++;
+      }
+      __syncthreads();
+      swap_slots(k, s, swp_a, swp_b, np);
+      nswp = np;
+    }
   }
+  if (nswp) swap_slots(k, s, swp_a, swp_b, nswp);   // back to the caller's slots
 #ifdef L0L2_PROF
   __syncthreads();
   if (tid < NW * 8) g_prof[blockIdx.x][tid / 8][tid % 8] += prof_s[tid / 8][tid % 8];
@@ -1172,6 +1253,8 @@ int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
   KP k{};
   k.act_mask = mask;
   k.prune_ub = a.prune_ub;
+  k.compact = 1;
+  if (const char* e = getenv("L0L2_COMPACT")) k.compact = atoi(e) != 0;   // tuning / test hook
   k.Z = c->Z; k.Lt = c->Lt;
   k.stt = c->stt; k.bchk = c->bchk;
   k.U = c->U; k.Ub = c->Ub; k.Upart = c->Upart; k.sums = c->sums; k.sums2 = c->sums2;

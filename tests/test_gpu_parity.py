@@ -135,6 +135,23 @@ def test_paired_equals_split_bitwise(case, monkeypatch):
     prob.close()
 
 
+def test_compaction_is_bitwise_invisible(case, monkeypatch):
+    """Node-slot compaction (≤ 8 active nodes spread over both halves are moved into half 0 for
+    single-half sweeps) changes no result bit: compare with compaction disabled."""
+    name, inst, lam0, lam2, M, P = case
+    prob = Problem(inst.X, inst.y, lam0, lam2, M, rho=P.rho, node_tol=1e-7, max_iters=800)
+    fx = _fixings(inst, 16, seed=8)
+    monkeypatch.setenv("L0L2_COMPACT", "1")
+    a = prob.l0l2_bound_batch(fx, want_dual_r=True)
+    monkeypatch.setenv("L0L2_COMPACT", "0")
+    b = prob.l0l2_bound_batch(fx, want_dual_r=True)
+    for key in ("warm_out", "lb", "primal", "iters", "branch_j", "flags", "dual_r"):
+        assert torch.equal(a[key], b[key]), key
+    it = a["iters"].cpu().numpy()
+    assert len(set(it.tolist())) > 1   # nodes retire at different checks
+    prob.close()
+
+
 def test_converged_bounds_and_decisions(case):
     """T3: converged LB / primal within 1e-6; LB ≤ independent relaxation optimum; iteration
     counts, branch index and support equal where the decisions are separated."""
