@@ -35,13 +35,21 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// c_j = X_jᵀ r for one column (lane-strided rows, fixed butterfly): every lane gets the sum
+// c_j = X_jᵀ r for one column (lane-strided rows, four independent accumulators so each lane keeps
+// four loads in flight, fixed combination order and butterfly): every lane gets the sum
 __device__ __forceinline__ double col_dot(const double* __restrict__ X, int64_t ld, int64_t n, int64_t j,
                                           const double* r, int lane) {
   const double* col = X + j * ld;
-  double a = 0.0;
-  for (int64_t i = lane; i < n; i += 32) a = fma(col[i], r[i], a);
-  return warp_sum(a);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t i = lane;
+  for (; i + 96 < n; i += 128) {
+    a0 = fma(__ldcs(col + i), r[i], a0);
+    a1 = fma(__ldcs(col + i + 32), r[i + 32], a1);
+    a2 = fma(__ldcs(col + i + 64), r[i + 64], a2);
+    a3 = fma(__ldcs(col + i + 96), r[i + 96], a3);
+  }
+  for (; i < n; i += 32) a0 = fma(__ldcs(col + i), r[i], a0);
+  return warp_sum((a0 + a1) + (a2 + a3));
 }
 
 __global__ void __launch_bounds__(MP_THREADS) mp_forward_scan(const double* __restrict__ X, int64_t ld, int64_t n,
@@ -178,7 +186,7 @@ int mp_run(Ctx* c, int max_rounds, cudaStream_t st, std::vector<int32_t>& S_out,
            double* obj, int* rounds_out) {
   const int64_t n = c->n, p = c->p;
   if (max_rounds <= 0) max_rounds = (int)std::min<int64_t>(4 * p + 10, 1 << 30);
-  const int grid = c->sms;
+  const int grid = 4 * c->sms;   // 32 warps per SM stream the columns
   // work space (allocated on first use, kept with the context)
   if (!c->mp_r) {
     c->mp_r = (double*)dalloc(c, sizeof(double) * n);
