@@ -354,6 +354,9 @@ def main():
                  "alg_bytes_per_launch": per_launch_bytes,
                  "alg_flops_per_launch": ks["admm_flops_alg"] / max(1, ks["admm_launches"]),
                  "share_of_step": ks["admm_ms"] / max(1e-9, ms / world if world > 1 else ms)})
+    upper = {"kernel": "fpg_kernel", "launches": ks["upper_launches"], "ms": ks["upper_ms"],
+             "gather_gbs_alg": ks["upper_bytes_alg"] / (ks["upper_ms"] / 1e3) / 1e9 if ks["upper_ms"] > 0 else 0.0,
+             "share_of_step": ks["upper_ms"] / max(1e-9, ms)}
     # root heuristic (Algorithm 3) on the same resident X: rounds × one X scan
     mp = None
     if world == 1:
@@ -444,7 +447,7 @@ def main():
                 "solve_status": st["status"], "rounds": st["rounds"], "max_open": st["max_open"],
                 "phase_s": {"bound": st["t_bound"], "upper": st["t_upper"], "tree": st["t_tree"], "comm": st["t_comm"]},
                 "create_s": t_create, "gpu_launches": int(launches),
-                "roofline": roof, "e2e": e2e, "clocks": clk.summary()}
+                "roofline": roof, "upper_bound_kernel": upper, "e2e": e2e, "clocks": clk.summary()}
         if certified is not None:
             line["certified_solves"] = certified
         if micro is not None:

@@ -207,6 +207,7 @@ typedef struct {
   double  admm_ms, admm_bytes_alg, admm_flops_alg;
   int64_t upper_launches;
   double  upper_ms;
+  double  upper_bytes_alg;  /* Σ 8·n·|S| over the supports: the X_S gather of the Gram build */
 } l0l2_kstats;
 int l0l2_kernel_stats(l0l2_ctx* ctx, l0l2_kstats* out, int32_t reset);
 

@@ -44,7 +44,7 @@ class _Stats(C.Structure):
 class _KStats(C.Structure):
     _fields_ = [("admm_launches", C.c_int64), ("admm_iters", C.c_int64), ("admm_node_iters", C.c_int64),
                 ("admm_ms", C.c_double), ("admm_bytes_alg", C.c_double), ("admm_flops_alg", C.c_double),
-                ("upper_launches", C.c_int64), ("upper_ms", C.c_double)]
+                ("upper_launches", C.c_int64), ("upper_ms", C.c_double), ("upper_bytes_alg", C.c_double)]
 
 
 _lib = None

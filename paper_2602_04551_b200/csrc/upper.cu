@@ -204,6 +204,7 @@ int upper_batch(Ctx* c, int B, const int64_t* supp_off, const int32_t* supp_idx,
   L0L2_CUDA(c, cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
   c->ks.upper_launches++;
   c->ks.upper_ms += ms;
+  c->ks.upper_bytes_alg += 8.0 * (double)c->n * (double)(off[B] - off[0]);   // X_S gathered once per support
   return L0L2_OK;
 }
 
