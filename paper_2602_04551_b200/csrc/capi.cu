@@ -75,6 +75,9 @@ void l0l2_destroy(l0l2_ctx* ctx) {
   for (void* p : c->owned) cudaFree(p);
   if (c->ub_scratch) cudaFree(c->ub_scratch);
   for (void* s : c->scr) if (s) cudaFree(s);
+  for (double* m : c->pool_chunks) cudaFree(m);
+  if (c->solve_buf) cudaFree(c->solve_buf);
+  if (c->solve_stream) cudaStreamDestroy(c->solve_stream);
   for (auto e : c->ev) if (e) cudaEventDestroy(e);
   comm_free(c);
   delete ctx;

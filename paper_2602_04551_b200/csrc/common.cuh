@@ -95,6 +95,13 @@ struct Ctx {
   void* nccl_comm = nullptr;
   NcclApi* nccl = nullptr;
   cudaStream_t comm_stream = nullptr;
+  // kept across l0l2_solve calls (allocation and stream creation are not free): the warm-state
+  // pool chunks, the round I/O block (sized for solve_buf_B nodes), the solve stream, the pool cap
+  std::vector<double*> pool_chunks;
+  void* solve_buf = nullptr;
+  int solve_buf_B = 0;
+  cudaStream_t solve_stream = nullptr;
+  size_t pool_cap = 0;
 };
 
 int set_err(Ctx* c, int code, const char* fmt, ...);

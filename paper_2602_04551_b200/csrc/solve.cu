@@ -102,27 +102,35 @@ struct NodeCmp {   // min-heap by (lb, id)
 };
 
 // Refcounted pool of parent (β, v) states, 2p doubles each, in HBM.
+// Refcounted parent warm states (2p doubles per slot) in chunks of HBM owned by the context and
+// reused by later solves (cudaMalloc/cudaFree of ~26 MB chunks per solve cost ~10% of a C4 step).
 struct SlotPool {
   Ctx* c = nullptr;
   int64_t p = 0;
   size_t cap = 0;
-  std::vector<double*> chunk;
   std::vector<int> freel, ref;
   static constexpr int kPerChunk = 16;
-  double* ptr(int s) const { return chunk[s / kPerChunk] + (int64_t)(s % kPerChunk) * 2 * p; }
+  std::vector<double*>& chunk() const { return c->pool_chunks; }
+  double* ptr(int s) const { return chunk()[s / kPerChunk] + (int64_t)(s % kPerChunk) * 2 * p; }
+  void adopt() {   // the chunks earlier solves left in the context: all slots free
+    for (size_t q = 0; q < chunk().size(); q++) add_slots();
+  }
+  void add_slots() {
+    const int base = (int)ref.size();
+    ref.resize(ref.size() + kPerChunk, 0);
+    for (int i = kPerChunk - 1; i >= 0; i--) freel.push_back(base + i);
+  }
   int alloc() {
     if (freel.empty()) {
-      if ((chunk.size() + 1) * kPerChunk > cap) return -1;
+      if ((chunk().size() + 1) * kPerChunk > cap) return -1;
       double* m = nullptr;
       if (cudaMalloc(&m, sizeof(double) * 2 * p * kPerChunk) != cudaSuccess) {
         cudaGetLastError();
-        cap = chunk.size() * kPerChunk;
+        cap = chunk().size() * kPerChunk;
         return -1;
       }
-      chunk.push_back(m);
-      const int base = (int)ref.size();
-      ref.resize(ref.size() + kPerChunk, 0);
-      for (int i = kPerChunk - 1; i >= 0; i--) freel.push_back(base + i);
+      chunk().push_back(m);
+      add_slots();
     }
     const int s = freel.back();
     freel.pop_back();
@@ -134,7 +142,6 @@ struct SlotPool {
     if (s < 0) return;
     if (--ref[s] == 0) freel.push_back(s);
   }
-  ~SlotPool() { for (double* m : chunk) cudaFree(m); }
 };
 
 // Per-round device I/O buffers
@@ -207,9 +214,26 @@ struct Solver {
     return id_base + (id_counter++) * W + R;
   }
 
+  // the round I/O buffers, carved from one context-owned block (reallocated only for a larger B)
   int alloc_bufs(int Bmax) {
     const int64_t p = c->p;
-    auto A = [&](size_t b) { return dalloc(c, b); };
+    size_t need = 0;
+    auto sz = [&](size_t b) { need += (b + 255) / 256 * 256; };
+    sz(sizeof(int64_t) * (Bmax + 1)); for (int i = 0; i < 4; i++) sz(sizeof(double) * Bmax);
+    for (int i = 0; i < 3; i++) sz(sizeof(int32_t) * Bmax);
+    sz(sizeof(int32_t) * (size_t)kBC * p); sz(sizeof(int64_t) * (Bmax + 1)); sz(Bmax); sz(sizeof(double*) * 2 * kBC);
+    if (c->solve_buf_B < Bmax) {
+      if (c->solve_buf) cudaFree(c->solve_buf);
+      c->solve_buf = nullptr;
+      c->solve_buf_B = 0;
+      if (cudaMalloc(&c->solve_buf, need) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(c, L0L2_ENOMEM, "solve buffers");
+      }
+      c->solve_buf_B = Bmax;
+    }
+    char* cur = (char*)c->solve_buf;
+    auto A = [&](size_t b) { void* r = cur; cur += (b + 255) / 256 * 256; return r; };
     d.fix_off = (int64_t*)A(sizeof(int64_t) * (Bmax + 1));
     d.parent_lb = (double*)A(sizeof(double) * Bmax);
     d.lb = (double*)A(sizeof(double) * Bmax);
@@ -617,16 +641,22 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
   S.W = c->nranks;
   S.R = c->rank;
   if (S.W > 1 && !c->nccl_comm) return set_err(c, L0L2_ENCCL, "communicator not initialised");
-  L0L2_CUDA(c, cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking));
-  struct StreamGuard { cudaStream_t s; ~StreamGuard() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } } } sg{S.st};
+  if (!c->solve_stream) L0L2_CUDA(c, cudaStreamCreateWithFlags(&c->solve_stream, cudaStreamNonBlocking));
+  S.st = c->solve_stream;
+  struct StreamGuard { cudaStream_t s; ~StreamGuard() { if (s) cudaStreamSynchronize(s); } } sg{S.st};
   S.pool.c = c;
   S.pool.p = c->p;
-  {
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    size_t capb = o.warm_bytes_cap > 0 ? (size_t)o.warm_bytes_cap : fr / 4;
-    S.pool.cap = std::max<size_t>(SlotPool::kPerChunk, capb / (sizeof(double) * 2 * c->p));
+  if (o.warm_bytes_cap > 0) {
+    S.pool.cap = std::max<size_t>(SlotPool::kPerChunk, (size_t)o.warm_bytes_cap / (sizeof(double) * 2 * c->p));
+  } else {
+    if (!c->pool_cap) {   // 25% of the HBM free at the first solve
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      c->pool_cap = std::max<size_t>(SlotPool::kPerChunk, fr / 4 / (sizeof(double) * 2 * c->p));
+    }
+    S.pool.cap = c->pool_cap;
   }
+  S.pool.adopt();
   c->trace.clear();
   if (o.record) S.trace = &c->trace;
   int rc = S.alloc_bufs(o.batch);
