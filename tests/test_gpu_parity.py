@@ -391,3 +391,24 @@ def test_solve_with_mp_incumbent(seed):
     assert list(res["support"]) == list(bf_S)
     assert res["obj"] <= mp["obj"] * (1 + 1e-12)
     prob.close()
+
+
+@pytest.mark.parametrize("n", [1008, 1060])
+def test_largest_n_classes(n):
+    """The two largest n classes of the ADMM kernel (n8 = 1008 and n8 ≤ 1064: most registers, least
+    shared-memory slack, fragment rows running past ld into the next stage) vs the oracle, with a
+    16+1-node batch (paired CTAs, compaction) and a fixed iteration count."""
+    inst = synth.make_instance(n, 168, 5, 0.3, 4.0, 31)
+    lam2 = 0.5
+    lam0 = synth.lambda0_rule(inst, lam2)
+    M = synth.bigM_rule(inst, lam2)
+    P = O.Problem(inst.X, inst.y, lam0, lam2, M)
+    prob = Problem(inst.X, inst.y, lam0, lam2, M, rho=P.rho, node_tol=-1.0, max_iters=23)
+    fx = _fixings(inst, 17, seed=4)
+    out = prob.l0l2_bound_batch(fx)
+    wo, lb = out["warm_out"].cpu().numpy(), out["lb"].cpu().numpy()
+    for k in (0, 7, 8, 15, 16):
+        r = O.admm_node(P, O.make_code(inst.p, *fx[k]), node_tol=-1.0, max_iters=23)
+        assert rel(wo[k, 0], r.beta) < 1e-9, (n, k)
+        assert abs(lb[k] - r.lb) <= 1e-9 * max(1.0, abs(r.lb))
+    prob.close()
