@@ -185,7 +185,8 @@ constexpr int PFD_DEFAULT = 1; // additional tiles prefetched into L2 beyond the
 constexpr int NMW = NW - 2;    // MMA warps (adjoint + forward); the last 2 warps run the epilogue
 constexpr int MMA_THREADS = NMW * 32;
 // n classes of the kernel: KS adjoint k-steps (4 rows) and MT forward row tiles (8 rows) per MMA
-// warp, so n8 ≤ min(4·NMW·KS, 8·NMW·MT).  (19, 10) is the largest: n ≤ 1064.  (16 MMA warps would
+// warp, so n8 ≤ min(4·NMW·KS, 8·NMW·MT).  (19, 10) is the largest class; the 3-stage tile ring then
+// caps n at 1056 (shared memory, checked in admm_alloc).  (16 MMA warps would
 // balance the 4 SM sub-partitions, but 18 warps leave 96 registers per thread: u and the forward
 // accumulators no longer fit.)
 constexpr int NCLS = 5;
@@ -1193,6 +1194,16 @@ int admm_alloc(Ctx* c) {
   L0L2_CUDA(c, cudaMemset(c->bar, 0, sizeof(unsigned) * 2));
   const size_t smem = admm_smem_bytes(ld);
   const AdmmKernel kern = admm_kernel(c->admm_cls);
+  {
+    // the 3-stage Z ring (24·ld doubles) must fit with everything else: n ≤ 1056 on B200
+    int optin = 0;
+    cudaFuncAttributes fa{};
+    L0L2_CUDA(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    L0L2_CUDA(c, cudaFuncGetAttributes(&fa, kern));
+    if (smem + fa.sharedSizeBytes > (size_t)optin)
+      return set_err(c, L0L2_EINVAL, "n = %lld needs %zu B of shared memory per CTA for the ADMM tile ring (> %d)",
+                     (long long)c->n, smem + fa.sharedSizeBytes, optin);
+  }
   L0L2_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int nblk = 0;
   L0L2_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, kern, kAdmmThreads, smem));
