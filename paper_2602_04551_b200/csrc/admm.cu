@@ -656,27 +656,31 @@ __device__ void reduce_u(const KP& k, Smem& s, double* dst) {
 // CTA g copies the segments of sub-range g.
 __device__ void compact_nonzeros(const KP& k, Smem& s, int* tot) {
   const int g = blockIdx.x, G = k.nsr;
-  __shared__ int off_s[kBC];
-  if (threadIdx.x < kBC) {
-    const int nd = threadIdx.x;
-    int off = 0, all = 0;
-    if (s.flags[nd] & F_ACTIVE)
-      for (int q = 0; q < G * NEW; q++) {   // segments in (sub-range, epilogue warp) order
-        const int c = __ldcg(k.seg_cnt + q * kBC + nd);
-        if (q < g * NEW) off += c;
-        all += c;
-      }
-    off_s[nd] = off;
-    tot[nd] = all;
+  __shared__ int off_s[kBC], all_s[kBC], own_s[NEW][kBC];
+  if (threadIdx.x < kBC) { off_s[threadIdx.x] = 0; all_s[threadIdx.x] = 0; }
+  __syncthreads();
+  // counts of all (sub-range, epilogue warp) segments, loaded by every thread in parallel; integer
+  // sums are exact in any order (shared-memory atomics)
+  for (int e = threadIdx.x; e < G * NEW * kBC; e += blockDim.x) {
+    const int q = e / kBC, nd = e % kBC;
+    if (!(s.flags[nd] & F_ACTIVE)) continue;
+    const int c = __ldcg(k.seg_cnt + e);
+    if (c) {
+      atomicAdd(&all_s[nd], c);
+      if (q < g * NEW) atomicAdd(&off_s[nd], c);
+    }
+    if (q >= g * NEW && q < (g + 1) * NEW) own_s[q - g * NEW][nd] = c;
   }
   __syncthreads();
+  if (threadIdx.x < kBC) tot[threadIdx.x] = (s.flags[threadIdx.x] & F_ACTIVE) ? all_s[threadIdx.x] : 0;
+  // this CTA's segments → the dense per-node lists at their offsets (segment order = column order)
   for (int w = 0; w < NEW; w++)
     for (int nd = 0; nd < kBC; nd++) {
       if (!(s.flags[nd] & F_ACTIVE)) continue;
       const int q = g * NEW + w;
-      const int c = __ldcg(k.seg_cnt + q * kBC + nd);
+      const int c = own_s[w][nd];
       int off = off_s[nd];
-      for (int ww = 0; ww < w; ww++) off += __ldcg(k.seg_cnt + (g * NEW + ww) * kBC + nd);
+      for (int ww = 0; ww < w; ww++) off += own_s[ww][nd];
       const int64_t so = ((int64_t)q * kBC + nd) * k.seg_cap;
       for (int r = threadIdx.x; r < c; r += blockDim.x)
         if (off + r < k.nz_cap) {
@@ -907,17 +911,37 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     }
     grid_sync(k.bar);
     PROF_ACC(5);
-    // every CTA derives the same per-node decision from the same partials (fixed order)
+    // every CTA derives the same per-node decision from the same partials in a fixed order: the
+    // sub-range partials of each (node, term) are summed in RCH fixed chunks in parallel, then the
+    // chunk sums in chunk order (a sequential 148-term loop per node was ~45 µs of L2 latency)
+    {
+      constexpr int RCH = 4;
+      double* cs = s.spart;   // [kBC][5][RCH]
+      const int Q = (int)gridDim.x;
+      if (tid < kBC * 5 * RCH) {
+        const int nd = tid / (5 * RCH), term = (tid / RCH) % 5, ch = tid % RCH;
+        double a = 0.0;
+        if (s.flags[nd] & F_ACTIVE) {
+          const int q0 = Q * ch / RCH, q1 = Q * (ch + 1) / RCH;
+#pragma unroll 8
+          for (int q = q0; q < q1; q++)
+            a += term < 4 ? __ldcg(k.sums + ((int64_t)q * kBC + nd) * kSums + term)
+                          : __ldcg(k.sums2 + (int64_t)q * kBC + nd);
+        }
+        cs[tid] = a;
+      }
+      __syncthreads();
+    }
     if (tid < kBC) {
       const int nd = tid;
       int fl = s.flags[nd];
       if (fl & F_ACTIVE) {
-        double T1 = 0, T2 = 0, T3 = 0, T4 = 0, T5 = 0;
-        for (int q = 0; q < (int)gridDim.x; q++) {
-          const double* sp = k.sums + ((int64_t)q * kBC + nd) * kSums;
-          T1 += __ldcg(sp + 0); T2 += __ldcg(sp + 1); T3 += __ldcg(sp + 2); T4 += __ldcg(sp + 3);
-          T5 += __ldcg(k.sums2 + (int64_t)q * kBC + nd);
+        double T[5];
+        for (int term = 0; term < 5; term++) {
+          const double* c4 = s.spart + (nd * 5 + term) * 4;
+          T[term] = (c4[0] + c4[1]) + (c4[2] + c4[3]);
         }
+        const double T1 = T[0], T2 = T[1], T3 = T[2], T4 = T[3], T5 = T[4];
         const double dual = 0.5 * k.yy - 0.5 * T1 - T2;
         const double primal = 0.5 * k.yy - T3 + 0.5 * T5 + T4;
         const double lbb = fmax(s.red[nd], dual);   // running max of checked duals (R7)
