@@ -292,9 +292,7 @@ __device__ void issue_stage_m(const KP& k, Smem& s, int m, int t0, int t1) {
   const int tile = m < t1 - t0 ? t0 + m : -1;
   s.stile[sg] = tile;
   if (tile >= 0) {
-#ifndef L0L2_NOFENCE
     fence_proxy_async_smem();
-#endif
     issue_stage(k, s, tile, sg);
     if (k.pfd > 0 && tile + k.pfd < t1) prefetch_l2(k.Z + (int64_t)(tile + k.pfd) * kPt * k.ld, tile_bytes(k));
   } else {
@@ -440,6 +438,9 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       const double* T = s.tiles + (size_t)(m % NST) * kPt * ld + cA * ld + kA;
       double sc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
+// EXP_NOADJ / EXP_NOFWD / EXP_NOEPI: timing experiments only (the results are wrong), built with
+// tools/build_variant.py — they compile out the adjoint DMMAs, the forward DMMAs or the epilogue math
+// to measure what the tile pipeline costs without them.
 #ifndef EXP_NOADJ
       for (int i = 0; i < KS; i++) dmma(sc[i & 3], T[4 * (warp + NMW * i)], uf[i]);
 #endif
