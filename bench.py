@@ -356,6 +356,8 @@ def main():
                  "share_of_step": ks["admm_ms"] / max(1e-9, ms / world if world > 1 else ms)})
     upper = {"kernel": "fpg_kernel", "launches": ks["upper_launches"], "ms": ks["upper_ms"],
              "gather_gbs_alg": ks["upper_bytes_alg"] / (ks["upper_ms"] / 1e3) / 1e9 if ks["upper_ms"] > 0 else 0.0,
+             "note": "X_S gather bytes (8·n·|S| per support) / the whole upper-bound time (multi-warp Gram pre-pass "
+                     "+ one-warp FPG iterations, which dominate: latency-bound, 0.1% of the step)",
              "share_of_step": ks["upper_ms"] / max(1e-9, ms)}
     # root heuristic (Algorithm 3) on the same resident X: rounds × one X scan
     mp = None

@@ -89,10 +89,26 @@ __global__ void __launch_bounds__(1024) mp_forward_apply(const double* __restric
                                                          double* beta, uint8_t* inS, int32_t* S, int* state,
                                                          double* log_delta) {
   __shared__ Cand best;
-  if (threadIdx.x == 0) {
-    Cand b = cand[0];
-    for (int q = 1; q < ncand; q++)
+  __shared__ Cand wb[32];
+  // argmin over the per-CTA candidates: the (Δ, j) lexicographic minimum is order independent, so a
+  // parallel tree gives the same winner as a sequential scan
+  {
+    Cand b{INFINITY, 0.0, 0x7fffffff};
+    for (int q = threadIdx.x; q < ncand; q += blockDim.x)
       if (cand_better(cand[q].delta, cand[q].j, b.delta, b.j)) b = cand[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Cand x{__shfl_xor_sync(0xffffffffu, b.delta, o), __shfl_xor_sync(0xffffffffu, b.b, o),
+             __shfl_xor_sync(0xffffffffu, b.j, o)};
+      if (cand_better(x.delta, x.j, b.delta, b.j)) b = x;
+    }
+    if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = b;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    Cand b = wb[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+      if (cand_better(wb[w].delta, wb[w].j, b.delta, b.j)) b = wb[w];
     best = b;
     state[2] = -1;
     if (b.delta < 0.0) {

@@ -28,6 +28,50 @@ __device__ __forceinline__ double warp_max(double x) {
   return x;
 }
 
+// Gram pre-pass: one CTA of nw warps per support; warp w accumulates Q = X_SᵀX_S over the row
+// chunks w, w + nw, ... (kRC rows each, staged in its shared slice), then the nw partials are summed
+// in warp order and 2λ2 added on the diagonal; Q (symmetric, s×s) → Qout[nd].  The X_S gather is
+// spread over nw warps instead of one (the FPG iterations themselves run on one warp).
+__global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ X, int64_t ld, int64_t n, double lam2,
+                                                  const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+                                                  double* __restrict__ Qout, int64_t qstride) {
+  extern __shared__ double sm[];
+  const int nd = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t o0 = off[nd];
+  const int s = (int)(off[nd + 1] - o0);
+  if (s == 0) return;
+  const int32_t* S = idx + o0;
+  double* Qp = sm + (int64_t)warp * (s * s + kRC * s);   // this warp's partial, then its staging
+  double* Xc = Qp + s * s;
+  for (int e = lane; e < s * s; e += 32) Qp[e] = 0.0;
+  __syncwarp();
+  for (int64_t r0 = (int64_t)warp * kRC; r0 < n; r0 += (int64_t)nw * kRC) {
+    const int rr = (int)((n - r0) < kRC ? (n - r0) : kRC);
+    for (int e = lane; e < rr * s; e += 32) {
+      const int a = e / rr, r = e % rr;
+      Xc[r * s + a] = X[(int64_t)S[a] * ld + r0 + r];
+    }
+    __syncwarp();
+    for (int e = lane; e < s * s; e += 32) {
+      const int a = e / s, b = e % s;
+      if (b < a) continue;
+      double acc = Qp[a * s + b];
+      for (int r = 0; r < rr; r++) acc = fma(Xc[r * s + a], Xc[r * s + b], acc);
+      Qp[a * s + b] = acc;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  double* Q = Qout + (int64_t)nd * qstride;
+  for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+    const int a = e / s, b = e % s;
+    const int u = a <= b ? a * s + b : b * s + a;   // upper-triangle entry
+    double v = 0.0;
+    for (int w = 0; w < nw; w++) v += sm[(int64_t)w * (s * s + kRC * s) + u];
+    Q[e] = v + (a == b ? 2.0 * lam2 : 0.0);
+  }
+}
+
 // one warp (one CTA) per support
 __global__ void __launch_bounds__(32) fpg_kernel(const double* __restrict__ X, int64_t ld, int64_t n,
                                                  const double* __restrict__ y, const double* __restrict__ c,
@@ -35,7 +79,7 @@ __global__ void __launch_bounds__(32) fpg_kernel(const double* __restrict__ X, i
                                                  const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
                                                  double* __restrict__ obj, double* __restrict__ beta_s,
                                                  double* __restrict__ Qglobal, int64_t qstride, int smax_smem,
-                                                 int max_iters) {
+                                                 int max_iters, const double* __restrict__ Qpre) {
   extern __shared__ double sm[];
   const int nd = blockIdx.x, lane = threadIdx.x;
   const int64_t o0 = off[nd];
@@ -55,7 +99,15 @@ __global__ void __launch_bounds__(32) fpg_kernel(const double* __restrict__ X, i
   double* bn = vec + 5 * s;   // trial β^{t+1}
   double* Xc = vec + 6 * s;   // [kRC][s] staging of X_S rows
 
-  // ---- Gram Q = X_SᵀX_S + 2λ2 I, staged kRC rows at a time (fixed summation order)
+  // ---- Gram Q = X_SᵀX_S + 2λ2 I: from the multi-warp pre-pass, or staged kRC rows at a time here
+  if (Qpre) {
+    const double* Qs = Qpre + (int64_t)nd * qstride;
+    if (s <= smax_smem) {
+      for (int e = lane; e < s * s; e += 32) Q[e] = Qs[e];
+    } else {
+      Q = const_cast<double*>(Qs);
+    }
+  } else {
   for (int e = lane; e < s * s; e += 32) Q[e] = 0.0;
   __syncwarp();
   for (int64_t r0 = 0; r0 < n; r0 += kRC) {
@@ -78,6 +130,7 @@ __global__ void __launch_bounds__(32) fpg_kernel(const double* __restrict__ X, i
     const int a = e / s, b = e % s;
     if (b < a) Q[a * s + b] = Q[b * s + a];
     else if (a == b) Q[a * s + b] += 2.0 * lam2;
+  }
   }
   for (int a = lane; a < s; a += 32) { q[a] = c[S[a]]; bb[a] = 0.0; bp[a] = 0.0; }
   __syncwarp();
@@ -190,13 +243,39 @@ int upper_batch(Ctx* c, int B, const int64_t* supp_off, const int32_t* supp_idx,
     Qg = (double*)c->ub_scratch;
     if (smem > limit) return set_err(c, L0L2_EINVAL, "support too large (%d)", smax);
   }
+  // multi-warp Gram pre-pass when nw ≥ 2 warps' partials fit shared memory
+  int gnw = 0;
+  for (int w = 8; w >= 2; w /= 2)
+    if (sizeof(double) * (size_t)w * ((size_t)smax * smax + (size_t)kRC * smax) <= limit) { gnw = w; break; }
+  const double* Qpre = nullptr;
+  if (gnw && smax > 0) {
+    const int64_t qs = (int64_t)smax * smax;
+    if (c->ub_scratch_bytes < (size_t)B * qs * sizeof(double)) {
+      if (c->ub_scratch) cudaFree(c->ub_scratch);
+      c->ub_scratch_bytes = (size_t)B * qs * sizeof(double);
+      if (cudaMalloc(&c->ub_scratch, c->ub_scratch_bytes) != cudaSuccess) {
+        c->ub_scratch = nullptr;
+        c->ub_scratch_bytes = 0;
+        return set_err(c, L0L2_ENOMEM, "upper-bound Gram scratch");
+      }
+    }
+    qstride = qs;
+    Qg = nullptr;
+    Qpre = (const double*)c->ub_scratch;
+  }
   L0L2_CUDA(c, cudaFuncSetAttribute(fpg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit));
+  L0L2_CUDA(c, cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit));
   if (!c->ev[2]) {
     for (auto& e : c->ev) if (!e) L0L2_CUDA(c, cudaEventCreate(&e));
   }
   L0L2_CUDA(c, cudaEventRecord(c->ev[2], st));
+  if (Qpre) {
+    gram_kernel<<<B, 32 * gnw, sizeof(double) * (size_t)gnw * ((size_t)smax * smax + (size_t)kRC * smax), st>>>(
+        c->X, c->ld, c->n, c->lam2, supp_off, supp_idx, (double*)c->ub_scratch, qstride);
+    L0L2_LAUNCHED(c);
+  }
   fpg_kernel<<<B, 32, smem, st>>>(c->X, c->ld, c->n, c->y, c->c, c->yy, c->lam0, c->lam2, c->M, supp_off, supp_idx,
-                                  obj, beta_s, Qg, qstride, smax_smem, 50000);
+                                  obj, beta_s, Qg, qstride, smax_smem, 50000, Qpre);
   L0L2_LAUNCHED(c);
   L0L2_CUDA(c, cudaEventRecord(c->ev[3], st));
   L0L2_CUDA(c, cudaEventSynchronize(c->ev[3]));
