@@ -371,9 +371,14 @@ def main():
               "note": "one HBM pass over X (8np bytes) per round + O(|S|n) backward work; host reads one flag per round"}
     prob.close()
     del prob
-    micro = None
+    micro = micro3 = None
     if world == 1 and not args.no_microbench:
         micro = bound_microbench(inst, rho, local, args.micro_iters)
+        if args.config == "C4":   # SURVEY §8(d) asks for C3 too: Z = 80 MB, L2-resident
+            inst3, _ = load_instance("C3", args.seed)
+            rho3 = float(np.mean(np.einsum("ij,ij->j", inst3.X, inst3.X))) * args.rho_mult
+            micro3 = bound_microbench(inst3, rho3, local, args.micro_iters)
+            micro3["workload"] = "C3 (n=1000, p=1e4; Z is L2-resident): " + micro3["workload"]
 
     # ------------------------------------------------------------------ end-to-end arm (host buffers)
     import torch as _t
@@ -479,6 +484,8 @@ def main():
             line["certified_solves"] = certified
         if micro is not None:
             line["bound_microbench"] = micro
+        if micro3 is not None:
+            line["bound_microbench_c3"] = micro3
         if c4cert is not None:
             line["certified_c4"] = c4cert
             if last["stats"]["status"] > 1:
