@@ -95,7 +95,9 @@ int l0l2_create(const double* X, const double* y, int64_t n, int64_t p,
  *   out  iters     int32[B]          ADMM iterations run
  *   out  flags     uint8[B]          L0L2_FLAG_* bits
  * Returns L0L2_WNOTCONV if any node stopped at max_iters (its lb is still valid).
- * The per-node arithmetic is independent of B and of the other nodes (bitwise).
+ * The per-node arithmetic is independent of B and of the other nodes (bitwise).  Nodes run in
+ * groups of 16 per persistent kernel launch (two node halves on CTA pairs that share each Z tile
+ * through L2); the call blocks until all groups are done.
  */
 int l0l2_bound_batch(l0l2_ctx* ctx, int32_t B,
                      const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
@@ -108,7 +110,8 @@ int l0l2_bound_batch(l0l2_ctx* ctx, int32_t B,
  * For support S_k = supp_idx[supp_off[k] .. supp_off[k+1]) (sorted, distinct) minimise
  * eq:upperboundbeta U_S(β) = ½‖y − X_Sβ‖² + λ2‖β‖² s.t. |β_i| ≤ M by the fast proximal
  * gradient method with Nesterov extrapolation t/(t+3) and Armijo backtracking
- * (eq:fpg_extrapolate..eq:fpg_armijo), batched one CTA per support.
+ * (eq:fpg_extrapolate..eq:fpg_armijo), batched one CTA per support (Gram
+ * Q = X_SᵀX_S + 2λ2I by a multi-warp pre-pass, then the iterations in support space).
  * DEVICE pointers, ordered on `stream`:
  *   in  supp_off int64[B+1], supp_idx int32[nnz]
  *   out obj      double[B]     U_S(β) + λ0|S|  (objective of eq:perspective at z = 1_S)
