@@ -182,7 +182,12 @@ __device__ __forceinline__ double nu_f(const KP& k, double x, uint8_t code) {   
 #endif
 constexpr int NST = L0L2_NST;  // Z tile stages in the TMA ring (3 × 64.75 KB at n = 1000)
 constexpr int PFD_DEFAULT = 1; // additional tiles prefetched into L2 beyond the smem ring (k.pfd)
-constexpr int NMW = NW - 2;    // MMA warps (adjoint + forward); the last 2 warps run the epilogue
+#ifndef L0L2_NMW
+#define L0L2_NMW 14
+#endif
+constexpr int NMW = L0L2_NMW;  // MMA warps (adjoint + forward); warps NMW, NMW+1 run the epilogue
+                               // (with 12 MMA warps the last 2 warps idle during sweeps)
+static_assert(NMW + NEW <= NW, "warp roles");
 constexpr int MMA_THREADS = NMW * 32;
 // n classes of the kernel: KS adjoint k-steps (4 rows) and MT forward row tiles (8 rows) per MMA
 // warp, so n8 ≤ min(4·NMW·KS, 8·NMW·MT).  (19, 10) is the largest class; the 3-stage tile ring then
@@ -190,8 +195,13 @@ constexpr int MMA_THREADS = NMW * 32;
 // balance the 4 SM sub-partitions, but 18 warps leave 96 registers per thread: u and the forward
 // accumulators no longer fit.)
 constexpr int NCLS = 5;
+#if L0L2_NMW == 12
+constexpr int CLS_KS[NCLS] = {2, 6, 10, 16, 22};
+constexpr int CLS_MT[NCLS] = {1, 3, 5, 8, 11};
+#else
 constexpr int CLS_KS[NCLS] = {2, 5, 10, 18, 19};
 constexpr int CLS_MT[NCLS] = {1, 3, 5, 9, 10};
+#endif
 
 // Per-stage copy of the epilogue's operands for tile J, TMA'd with Z_J on the same mbarrier:
 //   β_J [8][kBC], v_J [8][kBC], c_J [8], code_J [8][kBC] bytes (node-minor, as in HBM; a CTA
@@ -366,6 +376,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
   const int g = blockIdx.x;
   constexpr bool fused = (MODE == SW_FUSED);
   const bool is_mma = warp < NMW;
+  const bool is_epi = warp >= NMW && warp < NMW + NEW;
   if (s.sched[8]) {   // deferred start (prefill); a grid barrier has passed.  (sched[8] is rewritten
                       // only by the next prefill, so every thread takes this branch.)
     if (tid == 0) {
@@ -498,7 +509,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
     }
     if (!flushed) flush(sr0);
     flush(paired ? sr0 + 1 : sr0);
-  } else {
+  } else if (is_epi) {
     // ---------------- epilogue warps: element (j = et>>3, node = 8h + (et&7)) of each 8×8 block
     const int et = tid - MMA_THREADS, j = et >> 3, nd = et & 7, node = 8 * h + nd;
     const bool active = (s.flags[node] & F_ACTIVE) != 0;
