@@ -646,8 +646,18 @@ __device__ void reduce_u(const KP& k, Smem& s, double* dst) {
       const int64_t nd = e / k.n8, row = e % k.n8;
       const double* src = k.Upart + nd * k.ld + row;
       const int64_t qs = (int64_t)kBC * k.ld;
+      // all partials of the chunk in flight at once (the sum stays in q order)
+      constexpr int MAXQ = 20;
+      if (q1 - q0 <= MAXQ) {
+        double v[MAXQ];
+#pragma unroll
+        for (int i = 0; i < MAXQ; i++) v[i] = (q0 + i < q1) ? __ldcg(src + (int64_t)(q0 + i) * qs) : 0.0;
+#pragma unroll
+        for (int i = 0; i < MAXQ; i++) a += v[i];
+      } else {
 #pragma unroll 8
-      for (int q = q0; q < q1; q++) a += __ldcg(src + q * qs);
+        for (int q = q0; q < q1; q++) a += __ldcg(src + q * qs);
+      }
     }
     s.spart[c * RED_E + el] = a;
     __syncthreads();
