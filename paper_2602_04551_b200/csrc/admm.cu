@@ -733,7 +733,7 @@ __device__ void gather_partial(const KP& k, Smem& s, const int* tot) {
         const int32_t* ix = k.nz_idx + (int64_t)nd * k.nz_cap;
         const double* vx = k.nz_val + (int64_t)nd * k.nz_cap;
         const int nr = (int)(i1 - r0 < 8 ? i1 - r0 : 8);
-#pragma unroll 2
+#pragma unroll 8
         for (int e = slot; e < cnt; e += 64) {
           const double bv = __ldcg(vx + e);
           const double* col = k.X + (int64_t)__ldcg(ix + e) * k.ld + r0;

@@ -2,7 +2,8 @@ import sys, numpy as np, torch
 sys.path.insert(0, ".")
 import synth
 from paper_2602_04551_b200 import Problem
-inst = synth.config_instance("C4", seed=0)
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
+inst = synth.config_instance(cfg, seed=0)
 rho = 3.0 * float(np.mean(np.einsum("ij,ij->j", inst.X, inst.X)))
 fx = [((), ())] + synth.random_fixings(inst.p, 15, seed=11, depth_lo=5, depth_hi=10, prefer=inst.support_true)
 for ce in (10, 20, 1000):
