@@ -420,3 +420,34 @@ def test_largest_n_classes(n):
         assert rel(wo[k, 0], r.beta) < 1e-9, (n, k)
         assert abs(lb[k] - r.lb) <= 1e-9 * max(1.0, abs(r.lb))
     prob.close()
+
+
+@pytest.mark.parametrize("variant", ["lambda0_zero", "box_inactive", "box_tight"])
+def test_degenerate_penalties(variant):
+    """Degenerate penalty settings of eq:perspective: λ0 = 0 (no ℓ0 term: ψ is the pure ridge
+    branch, ẑ ∈ {0, 1}), M ≫ ‖β‖∞ (box never active), M tiny (box active on most coordinates).
+    Fixed-iteration ADMM state vs the oracle, and the certified solve = brute force."""
+    inst = synth.make_instance(40, 12, 3, 0.2, 4.0, 2)   # p = 12: brute force in milliseconds
+    lam2 = 0.05
+    lam0, M = synth.lambda0_rule(inst, lam2), synth.bigM_rule(inst, lam2)
+    if variant == "lambda0_zero":
+        lam0 = 0.0
+    elif variant == "box_inactive":
+        M = 1e3
+    else:
+        M = 0.05
+    P = O.Problem(inst.X, inst.y, lam0, lam2, M)
+    prob = Problem(inst.X, inst.y, lam0, lam2, M, rho=P.rho, node_tol=-1.0, max_iters=37)
+    fx = _fixings(inst, 5, seed=2)
+    out = prob.l0l2_bound_batch(fx)
+    wo, lb = out["warm_out"].cpu().numpy(), out["lb"].cpu().numpy()
+    for k, (F0, F1) in enumerate(fx):
+        r = O.admm_node(P, O.make_code(inst.p, F0, F1), node_tol=-1.0, max_iters=37)
+        assert rel(wo[k, 0], r.beta) < 1e-9, (variant, k)
+        assert abs(lb[k] - r.lb) <= 1e-9 * max(1.0, abs(r.lb))
+    prob.close()
+    bf_obj, bf_S, _ = O.brute_force(P)
+    prob = Problem(inst.X, inst.y, lam0, lam2, M, rho=P.rho, node_tol=1e-10, max_iters=20000)
+    res = prob.l0l2_solve(gap_tol=1e-9, batch=8)
+    assert abs(res["obj"] - bf_obj) <= 1e-8 * max(1.0, abs(bf_obj)), (variant, res["obj"], bf_obj)
+    prob.close()
