@@ -22,6 +22,14 @@ __device__ __forceinline__ double warp_sum(double x) {
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   return x;
 }
+// several independent sums in one butterfly (the shuffle latencies overlap)
+template <int K>
+__device__ __forceinline__ void warp_sum_k(double (&x)[K]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < K; i++) x[i] += __shfl_xor_sync(0xffffffffu, x[i], o);
+}
 __device__ __forceinline__ double warp_max(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
@@ -159,8 +167,12 @@ __global__ void __launch_bounds__(32) fpg_kernel(const double* __restrict__ X, i
       bg = fma(bt[a], ga, bg);
     }
     __syncwarp();
-    qb = warp_sum(qb);
-    bg = warp_sum(bg);
+    {
+      double r2[2] = {qb, bg};
+      warp_sum_k<2>(r2);
+      qb = r2[0];
+      bg = r2[1];
+    }
     const double f_t = 0.5 * bg - 0.5 * qb;     // ½β̃ᵀ(Qβ̃ − q) − ½qᵀβ̃
     double alpha = alpha0, f_n = 0.0;
     for (int ls = 0; ls < 60; ls++) {
@@ -180,10 +192,14 @@ __global__ void __launch_bounds__(32) fpg_kernel(const double* __restrict__ X, i
         qn = fma(q[a], bn[a], qn);
         nQn = fma(bn[a], r, nQn);
       }
-      gd = warp_sum(gd);
-      dd = warp_sum(dd);
-      qn = warp_sum(qn);
-      nQn = warp_sum(nQn);
+      {
+        double r4[4] = {gd, dd, qn, nQn};
+        warp_sum_k<4>(r4);
+        gd = r4[0];
+        dd = r4[1];
+        qn = r4[2];
+        nQn = r4[3];
+      }
       f_n = 0.5 * nQn - qn;
       const double rhs = f_t + gd + dd / (2.0 * alpha);
       if (f_n <= rhs + 1e-15 * fabs(rhs)) break;   // eq:fpg_armijo (rounding slack)
@@ -197,8 +213,11 @@ __global__ void __launch_bounds__(32) fpg_kernel(const double* __restrict__ X, i
       bb[a] = bn[a];
     }
     __syncwarp();
-    dmax = warp_max(dmax);
-    bmax = warp_max(bmax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+      bmax = fmax(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+    }
     f_cur = f_n;
     if (dmax <= 1e-14 * (1.0 + bmax)) break;   // change in β_S below tolerance
   }
