@@ -142,6 +142,47 @@ __global__ void __launch_bounds__(32) fpg_kernel(const double* __restrict__ X, i
   }
   for (int a = lane; a < s; a += 32) { q[a] = c[S[a]]; bb[a] = 0.0; bp[a] = 0.0; }
   __syncwarp();
+  // warm start (R12): β⁰ = Proj_[−M,M](Q⁻¹q) by a Cholesky factor of the s×s Gram in the
+  // staging area (s ≤ 32).  When the box is inactive this is the minimiser and FPG stops after one
+  // step; otherwise FPG continues from it.  The FPG iterations are the paper's.
+  if (s <= 32) {
+    double* Lf = Xc;   // [s][s] lower factor (kRC·s ≥ s² doubles for s ≤ kRC)
+    for (int j = 0; j < s; j++) {
+      double d = 0.0;
+      if (lane == j) {
+        d = Q[j * s + j];
+        for (int k2 = 0; k2 < j; k2++) d -= Lf[j * s + k2] * Lf[j * s + k2];
+        Lf[j * s + j] = sqrt(d);
+      }
+      __syncwarp();
+      if (lane > j && lane < s) {
+        double v = Q[lane * s + j];
+        for (int k2 = 0; k2 < j; k2++) v -= Lf[lane * s + k2] * Lf[j * s + k2];
+        Lf[lane * s + j] = v / Lf[j * s + j];
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      double* z = bt;   // forward L z = q, then back Lᵀ x = z (x in bn)
+      for (int i = 0; i < s; i++) {
+        double v = q[i];
+        for (int k2 = 0; k2 < i; k2++) v -= Lf[i * s + k2] * z[k2];
+        z[i] = v / Lf[i * s + i];
+      }
+      for (int i = s - 1; i >= 0; i--) {
+        double v = z[i];
+        for (int k2 = i + 1; k2 < s; k2++) v -= Lf[k2 * s + i] * bn[k2];
+        bn[i] = v / Lf[i * s + i];
+      }
+    }
+    __syncwarp();
+    for (int a = lane; a < s; a += 32) {
+      const double b0 = fmin(fmax(bn[a], -M), M);
+      bb[a] = b0;
+      bp[a] = b0;
+    }
+    __syncwarp();
+  }
   // Gershgorin bound on λmax(Q) → initial step α0 = 1/L̂ (R12)
   double Lh = 0.0;
   for (int a = lane; a < s; a += 32) {
