@@ -61,7 +61,9 @@ struct KP {
   int* nodei;                      // [kBC][2]: flags, iters
   unsigned* bar;                   // [2]: count, generation
   double* out_lb; double* out_primal; int* out_iters; uint8_t* out_flags;
-  int64_t ld, n, n8, p8;
+  int64_t ld, n, n8, p8;           // streamed operand (Z, or D in the direct regime): ld, rows, rows/8·8
+  int64_t xld, xn;                  // X (sparse primal gather) and Lᵀ: leading dimension, rows
+  int direct;                       // direct regime (R17): b = D w, w⁺ written to U, no forward / reduction
   int ntiles, nsr, nb, check_every, max_iters, pfd;   // nsr: tile sub-ranges (= grid)
   unsigned act_mask;               // node slots run by this launch (outputs written for these only)
   double prune_ub;                 // early prune threshold (R16; +inf = off)
@@ -392,6 +394,10 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
   const int sr0 = paired ? (g & ~1) : g;
   const int tb = paired ? sub_t(k, sr0 + 1) : 0x7fffffff;   // first tile of the second sub-range
   const int t0s = s.sched[6], t1s = s.sched[7];               // this sweep's tile range
+  // direct regime (R17): this sweep reads w from uin and writes w⁺ to uout (double-buffered by
+  // sweep parity; a CTA may finish its tiles while another still loads its u fragments)
+  const double* uin = (k.direct && (s.sched[0] & 1)) ? k.Ub : k.U;
+  double* uout = (k.direct && (s.sched[0] & 1)) ? k.U : k.Ub;
   // wait for ring stage m; returns its tile (−1: the CTA's sweep is over)
   auto stage = [&](int m) {
     const int sg = m % NST;
@@ -420,7 +426,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
 #pragma unroll
     for (int i = 0; i < KS; i++) {
       const int q = warp + NMW * i;
-      uf[i] = (fused && uact && q < kt) ? __ldcg(k.U + (8 * h + cA) * ld + q * 4 + kA) : 0.0;
+      uf[i] = (fused && uact && q < kt) ? __ldcg(uin + (8 * h + cA) * ld + q * 4 + kA) : 0.0;
     }
     // this CTA's forward partial of sub-range sr: Upart[sr][8h + node][row]; then restart
     auto flush = [&](int sr) {
@@ -470,7 +476,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       const int sg = m % NST;
       const bool nxt = fused ? adjoint(m + 1) : true;
       PROF_T0();
-      if (!flushed && ctile >= tb) { flush(sr0); flushed = true; }
+      if (!flushed && ctile >= tb && !k.direct) { flush(sr0); flushed = true; }
       mbar_wait(&s.wready[m & 1], (hph >> (m & 1)) & 1u);   // w⁺_J(m) published
       hph ^= 1u << (m & 1);
       PROF_ACC(2);
@@ -482,10 +488,12 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       // two passes (k = cols 0-3, then 4-7), so consecutive DMMAs never share an accumulator (the
       // asm volatile DMMAs issue in source order; back-to-back dependent pairs stalled on latency)
 #ifndef EXP_NOFWD
+      if (!k.direct) {
 #pragma unroll
-      for (int i = 0; i < MT; i++) dmma(acc[i], T[8 * (warp + NMW * i)], b0);            // A[m = row][k = col j]
+        for (int i = 0; i < MT; i++) dmma(acc[i], T[8 * (warp + NMW * i)], b0);          // A[m = row][k = col j]
 #pragma unroll
-      for (int i = 0; i < MT; i++) dmma(acc[i], T[4 * ld + 8 * (warp + NMW * i)], b1);
+        for (int i = 0; i < MT; i++) dmma(acc[i], T[4 * ld + 8 * (warp + NMW * i)], b1);
+      }
 #endif
       PROF_ACC(3);
       if (!fused) mbar_arrive_warp(&s.sready[m & 1]);   // w⁺ buffer m&1 free again
@@ -507,8 +515,10 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       if (fused) { cur = nxt; ctile = ntile; }
       else { ctile = stage(m + 1); cur = ctile >= 0; }
     }
-    if (!flushed) flush(sr0);
-    flush(paired ? sr0 + 1 : sr0);
+    if (!k.direct) {
+      if (!flushed) flush(sr0);
+      flush(paired ? sr0 + 1 : sr0);
+    }
   } else if (is_epi) {
     // ---------------- epilogue warps: element (j = et>>3, node = 8h + (et&7)) of each 8×8 block
     const int et = tid - MMA_THREADS, j = et >> 3, nd = et & 7, node = 8 * h + nd;
@@ -568,12 +578,14 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
         const double sv = part[0];
         double bnz = 0.0;
         if (active) {
-          const double b = (w - sv) * k.inv_rho;               // b = D w, D = (I − ZᵀZ)/ρ (R1)
+          // b = D w: Z-form D = (I − ZᵀZ)/ρ (R1) with sv = (ZᵀZ w)_j, or direct with sv = (D w)_j
+          const double b = k.direct ? sv : (w - sv) * k.inv_rho;
           const double bn = refresh ? q_beta : prox(k, b + vr, q_code);
           const double vn = q_v + k.rho * (b - bn);
           if (check) {
-            sT1 = fma(b, sv, sT1);
-            sT2 += nu_f(k, fabs(q_c - sv), q_code);
+            const double xxb = k.direct ? w - k.rho * b : sv;   // (XᵀX b)_j, since (XᵀX + ρI) b = w
+            sT1 = fma(b, xxb, sT1);
+            sT2 += nu_f(k, fabs(q_c - xxb), q_code);
             sT3 = fma(q_c, bn, sT3);
             sT4 += psi_f(k, bn, q_code);
             k.bchk[e] = b;
@@ -599,6 +611,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       }
 #endif
       s.Ws[(m & 1) * 8 * 12 + nd * 12 + j] = wn;
+      if (k.direct) uout[(int64_t)node * k.ld + col0 + j] = wn;   // the next sweep's w (R17)
       mbar_arrive_warp(&s.wready[m & 1]);
       PROF_ACC(5);
     }
@@ -719,7 +732,7 @@ __device__ void compact_nonzeros(const KP& k, Smem& s, int* tot) {
 // deterministic and independent of the batch.
 __device__ void gather_partial(const KP& k, Smem& s, const int* tot) {
   const int g = blockIdx.x, G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t i0 = k.n * g / G, i1 = k.n * (g + 1) / G;
+  const int64_t i0 = k.xn * g / G, i1 = k.xn * (g + 1) / G;
   const int nl = warp >> 1, slot = (warp & 1) * 32 + lane;
   double* red = s.spart;   // [8][2][8]
   double part = 0.0;       // thread tid < kBC: node tid
@@ -736,7 +749,7 @@ __device__ void gather_partial(const KP& k, Smem& s, const int* tot) {
 #pragma unroll 8
         for (int e = slot; e < cnt; e += 64) {
           const double bv = __ldcg(vx + e);
-          const double* col = k.X + (int64_t)__ldcg(ix + e) * k.ld + r0;
+          const double* col = k.X + (int64_t)__ldcg(ix + e) * k.xld + r0;
 #pragma unroll
           for (int r = 0; r < 8; r++)
             if (r < nr) a[r] = fma(bv, __ldg(col + r), a[r]);
@@ -771,7 +784,7 @@ __device__ void gather_partial(const KP& k, Smem& s, const int* tot) {
 __device__ void lmatvec_partial(const KP& k, Smem& s) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = blockIdx.x, G = gridDim.x;
-  const int64_t i0 = k.n * g / G, i1 = k.n * (g + 1) / G;
+  const int64_t i0 = k.xn * g / G, i1 = k.xn * (g + 1) / G;
   double part[kBC];
 #pragma unroll
   for (int nd = 0; nd < kBC; nd++) part[nd] = 0.0;
@@ -779,11 +792,11 @@ __device__ void lmatvec_partial(const KP& k, Smem& s) {
     double a[kBC];
 #pragma unroll
     for (int nd = 0; nd < kBC; nd++) a[nd] = 0.0;
-    const double* lrow = k.Lt + i * k.ld;    // row i of L = column i of Lᵀ, entries m ≤ i
+    const double* lrow = k.Lt + i * k.xld;   // row i of L = column i of Lᵀ, entries m ≤ i
     for (int64_t m = lane; m <= i; m += 32) {
       const double l = lrow[m];
 #pragma unroll
-      for (int nd = 0; nd < kBC; nd++) a[nd] = fma(l, __ldcg(k.Ub + nd * k.ld + m), a[nd]);
+      for (int nd = 0; nd < kBC; nd++) a[nd] = fma(l, __ldcg(k.Ub + nd * k.xld + m), a[nd]);
     }
 #pragma unroll
     for (int nd = 0; nd < kBC; nd++) {
@@ -836,11 +849,12 @@ __device__ void swap_slots(const KP& k, Smem& s, const int* pa, const int* pb, i
     t = H[a]; H[a] = H[b]; H[b] = t;
   }
   const int64_t r0 = k.n8 * g / G, r1 = k.n8 * (g + 1) / G;
+  double* Ucur = (k.direct && (s.sched[0] & 1)) ? k.Ub : k.U;   // the buffer the next sweep reads
   for (int64_t e = tid; e < (r1 - r0) * np; e += blockDim.x) {
     const int q = (int)(e % np);
     const int64_t row = r0 + e / np;
-    double* ua = k.U + (int64_t)pa[q] * k.ld + row;
-    double* ub = k.U + (int64_t)pb[q] * k.ld + row;
+    double* ua = Ucur + (int64_t)pa[q] * k.ld + row;
+    double* ub = Ucur + (int64_t)pb[q] * k.ld + row;
     const double t = *ua; *ua = *ub; *ub = t;
   }
   fence_proxy_async_global();   // the next sweep reads the state blocks with TMA
@@ -895,11 +909,11 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   // u0 = Z (c + ρβ0 − v0), then the warm/cold refresh sweep (R6)
   sweep<SW_FWD_W, KS, MT>(k, s, false, false, phases, hph);
   grid_sync(k.bar);
-  reduce_u(k, s, k.U);
+  if (!k.direct) reduce_u(k, s, k.U);
   grid_sync(k.bar);
   sweep<SW_FUSED, KS, MT>(k, s, true, false, phases, hph);
   grid_sync(k.bar);
-  reduce_u(k, s, k.U);
+  if (!k.direct) reduce_u(k, s, k.U);
   grid_sync(k.bar);
 
   for (int it = 1; it <= k.max_iters; it++) {
@@ -908,7 +922,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     sweep<SW_FUSED, KS, MT>(k, s, false, chk, phases, hph);
     PROF_ACC(6);
     grid_sync(k.bar);
-    reduce_u(k, s, k.U);
+    if (!k.direct) reduce_u(k, s, k.U);
     __shared__ int tot_s[kBC];
     if (chk) compact_nonzeros(k, s, tot_s);   // β⁺'s nonzeros → dense per-node lists
     grid_sync(k.bar);
@@ -1197,8 +1211,10 @@ size_t admm_smem_bytes(int64_t ld) {
 }
 
 int admm_alloc(Ctx* c) {
-  const int64_t p8 = round8(c->p), ld = c->ld;
-  c->admm_cls = admm_class(round8(c->n));
+  // the streamed operand: Z (n×p, ld) or, in the direct regime, D (p×p, ldD)
+  const int64_t p8 = round8(c->p), ld = c->direct ? c->ldD : c->ld;
+  const int64_t kn = c->direct ? c->p : c->n;
+  c->admm_cls = admm_class(round8(kn));
   if (c->admm_cls < 0)
     return set_err(c, L0L2_EINVAL, "n = %lld > %d not supported by the fused ADMM kernel", (long long)c->n,
                    std::min(4 * NMW * CLS_KS[NCLS - 1], 8 * NMW * CLS_MT[NCLS - 1]));
@@ -1222,6 +1238,7 @@ int admm_alloc(Ctx* c) {
   // dense per-node lists (capacity p/16: above it the forward-only Zβ sweep is cheaper)
   c->seg_cap = (int)((ntiles + c->grid - 1) / c->grid) * (kPt / NEW);   // columns per (CTA, epilogue warp)
   c->nz_cap = (int)std::max<int64_t>(256, round8(c->p) / 16);
+  if (c->direct) c->nz_cap = (int)round8(c->p);   // no dense fallback (it needs Z): every β⁺ is gathered
   c->seg_idx = (int32_t*)dalloc(c, sizeof(int32_t) * c->grid * NEW * kBC * c->seg_cap);
   c->seg_val = (double*)dalloc(c, sizeof(double) * c->grid * NEW * kBC * c->seg_cap);
   c->seg_cnt = (int*)dalloc(c, sizeof(int) * c->grid * NEW * kBC);
@@ -1315,7 +1332,11 @@ int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
   k.prune_ub = a.prune_ub;
   k.compact = 1;
   if (const char* e = getenv("L0L2_COMPACT")) k.compact = atoi(e) != 0;   // tuning / test hook
-  k.Z = c->Z; k.Lt = c->Lt;
+  k.Z = c->direct ? c->D : c->Z;
+  k.Lt = c->Lt;
+  k.direct = c->direct;
+  k.xld = c->ld;
+  k.xn = c->n;
   k.stt = c->stt; k.bchk = c->bchk;
   k.U = c->U; k.Ub = c->Ub; k.Upart = c->Upart; k.sums = c->sums; k.sums2 = c->sums2;
   k.nodef = c->node_f; k.nodei = c->node_i; k.bar = c->bar;
@@ -1323,7 +1344,10 @@ int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
   k.X = c->X; k.seg_cap = c->seg_cap; k.nz_cap = c->nz_cap;
   if (const char* e = getenv("L0L2_NZCAP")) k.nz_cap = std::min(k.nz_cap, atoi(e));   // testing hook (0 = always sweep)
   k.out_lb = a.lb; k.out_primal = a.primal; k.out_iters = a.iters; k.out_flags = a.flags;
-  k.ld = c->ld; k.n = c->n; k.n8 = round8(c->n); k.p8 = round8(c->p);
+  k.ld = c->direct ? c->ldD : c->ld;
+  k.n = c->direct ? c->p : c->n;
+  k.n8 = round8(k.n);
+  k.p8 = round8(c->p);
   k.pfd = PFD_DEFAULT;
   k.pfs = 0;
   if (const char* e = getenv("L0L2_PFS")) k.pfs = std::max(0, atoi(e));   // tuning hook
@@ -1345,7 +1369,7 @@ int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
   k.psi_4 = c->lam0 / c->M + c->lam2 * c->M;
   void* args[] = {&k};
   L0L2_CUDA(c, cudaLaunchCooperativeKernel((void*)admm_kernel(c->admm_cls), dim3(c->grid), dim3(kAdmmThreads), args,
-                                           admm_smem_bytes(c->ld), st));
+                                           admm_smem_bytes(k.ld), st));
   L0L2_LAUNCHED(c);
   return L0L2_OK;
 }
@@ -1367,13 +1391,16 @@ int account_admm(Ctx* c, int nb, const int* iters_host) {
   const int nl = split ? 2 : 1;
   double T = 0.0;
   for (int l = 0; l < nl; l++) T += (double)(tmax[l] + 1);
-  const double n = (double)c->n, p = (double)c->p;
+  // per iteration one read of the streamed operand (Z: n×p, or D: p×p in the direct regime) and the
+  // node state; flops per node-iteration 4np (Zᵀ(Zw)) or 2p² (Dw)
+  const double p = (double)c->p, kn = c->direct ? p : (double)c->n;
+  const double fl = c->direct ? 2.0 * p * p : 4.0 * kn * p;
   c->ks.admm_launches += nl;
   c->ks.admm_iters += (int64_t)T;
   c->ks.admm_node_iters += tsum;
   c->ks.admm_ms += ms;
-  c->ks.admm_bytes_alg += T * 8.0 * n * p + 33.0 * p * (double)(tsum + nb);
-  c->ks.admm_flops_alg += (double)(tsum + nb) * 4.0 * n * p;
+  c->ks.admm_bytes_alg += T * 8.0 * kn * p + 33.0 * p * (double)(tsum + nb);
+  c->ks.admm_flops_alg += (double)(tsum + nb) * fl;
   return L0L2_OK;
 }
 

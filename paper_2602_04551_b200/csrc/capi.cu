@@ -170,6 +170,10 @@ int l0l2_create(const double* X, const double* y, int64_t n, int64_t p, double l
     }
   }
   if (ok) {
+    // direct regime (R17): b = D w with the p×p D when p ≤ 2n and D's tile ring fits
+    c->ldD = padded_ld(c->p);
+    c->direct = (c->p <= 2 * c->n && c->ldD <= padded_ld(1056)) ? 1 : 0;
+    if (const char* e = getenv("L0L2_DIRECT")) c->direct = c->direct && atoi(e) != 0;   // test / tuning hook
     rc = precompute(c, st);
     ok = rc == L0L2_OK;
   }

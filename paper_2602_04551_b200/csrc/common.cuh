@@ -39,6 +39,10 @@ struct Ctx {
   double yy = 0;                  // ‖y‖²
   // device data (owned)
   double *X = nullptr, *Z = nullptr, *y = nullptr, *c = nullptr, *colsq = nullptr, *L = nullptr, *Lt = nullptr;
+  // direct regime (p ≤ 2n and p ≤ 1056, R17): D = (XᵀX + ρI)⁻¹ = (I − ZᵀZ)/ρ, p×p, ld ldD
+  double *D = nullptr;
+  int64_t ldD = 0;
+  int direct = 0;
   // ADMM work space for one pass of kBC nodes
   double *stt = nullptr;                                    // node state, per-tile blocks (admm.cu)
   double *bchk = nullptr;                                   // [p][kBC]

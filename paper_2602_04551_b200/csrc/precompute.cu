@@ -208,6 +208,17 @@ int precompute(Ctx* c, cudaStream_t st) {
   L0L2_CUDA(c, cudaMemcpyAsync(&c->yy, d_yy, sizeof(double), cudaMemcpyDeviceToHost, st));
   L0L2_CUDA(c, cudaStreamSynchronize(st));
   if (h_info) return set_err(c, L0L2_EINVAL, "XXᵀ+ρI not positive definite at pivot %d", h_info - 1);
+  if (c->direct) {
+    // D = (I − ZᵀZ)/ρ = (XᵀX + ρI)⁻¹ (Woodbury, R1), p8 × p8 with zero padding
+    c->D = (double*)dalloc(c, sizeof(double) * c->ldD * p8);
+    if (!c->D) return set_err(c, L0L2_ENOMEM, "direct-regime D");
+    L0L2_CUDA(c, cudaMemsetAsync(c->D, 0, sizeof(double) * c->ldD * p8, st));
+    rc = gemm_f64(c, p8, p8, n, -1.0 / c->rho, c->Z, ld, true, c->Z, ld, false, 0.0, c->D, c->ldD, st);
+    if (rc) return rc;
+    add_diag<<<(unsigned)((p + 255) / 256), 256, 0, st>>>(c->D, c->ldD, p, 1.0 / c->rho);
+    L0L2_LAUNCHED(c);
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+  }
   return L0L2_OK;
 }
 

@@ -395,7 +395,7 @@ def test_solve_with_mp_incumbent(seed):
 
 def test_n_beyond_the_tile_ring_is_rejected():
     """n whose 3-stage Z tile ring does not fit one CTA's shared memory: a clean L0L2_EINVAL."""
-    inst = synth.make_instance(1064, 40, 3, 0.3, 4.0, 1)
+    inst = synth.make_instance(1064, 2200, 3, 0.3, 4.0, 1)   # p > 2n: Z-form (the direct regime streams D)
     with pytest.raises(L0L2Error) as e:
         Problem(inst.X, inst.y, 1.0, 0.5, 2.0)
     assert e.value.code == -1 and "shared memory" in str(e.value)
@@ -406,7 +406,7 @@ def test_largest_n_classes(n):
     """The two largest n classes of the ADMM kernel (n8 = 1008, and 1056 = the largest n whose tile
     ring fits: most registers, least shared-memory slack, fragment rows running past ld into the next
     stage) vs the oracle, with a 16+1-node batch (paired CTAs, compaction), fixed iterations."""
-    inst = synth.make_instance(n, 168, 5, 0.3, 4.0, 31)
+    inst = synth.make_instance(n, 2200, 5, 0.3, 4.0, 31)   # p > 2n: the Z-form kernel at its largest n classes
     lam2 = 0.5
     lam0 = synth.lambda0_rule(inst, lam2)
     M = synth.bigM_rule(inst, lam2)
@@ -451,3 +451,25 @@ def test_degenerate_penalties(variant):
     res = prob.l0l2_solve(gap_tol=1e-9, batch=8)
     assert abs(res["obj"] - bf_obj) <= 1e-8 * max(1.0, abs(bf_obj)), (variant, res["obj"], bf_obj)
     prob.close()
+
+
+def test_direct_regime_equals_zform(monkeypatch):
+    """R17: for p ≤ 2n the kernel streams D = (I − ZᵀZ)/ρ (p×p) instead of Z; same bounds (1e-9),
+    iteration counts and branches as the Z-form on the same nodes, and both vs the oracle."""
+    inst, lam0, lam2, M = _instance("direct")
+    P = O.Problem(inst.X, inst.y, lam0, lam2, M)
+    fx = _fixings(inst, 17, seed=6)
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("L0L2_DIRECT", mode)
+        prob = Problem(inst.X, inst.y, lam0, lam2, M, rho=P.rho, node_tol=1e-7, max_iters=3000)
+        outs[mode] = prob.l0l2_bound_batch(fx)
+        prob.close()
+    a, b = outs["1"], outs["0"]
+    la, lb_ = a["lb"].cpu().numpy(), b["lb"].cpu().numpy()
+    assert np.max(np.abs(la - lb_) / np.maximum(1.0, np.abs(lb_))) < 1e-9
+    assert torch.equal(a["iters"], b["iters"]) and torch.equal(a["branch_j"], b["branch_j"])
+    for k in (0, 9, 16):
+        r = O.admm_node(P, O.make_code(inst.p, *fx[k]), node_tol=1e-7, max_iters=3000)
+        assert abs(float(la[k]) - r.lb) <= 1e-6 * max(1.0, abs(r.lb))
+        assert int(a["iters"][k]) == r.iters
