@@ -27,6 +27,11 @@
 // check sums and nonzero lists are kept per sub-range and reduced across the grid in a fixed
 // order, so a node's arithmetic is bitwise the same in either mode, in any slot, for any B.
 //
+// Direct regime (p ≤ 2n, the paper's D branch P:374, R17): the same kernel streams the
+// tiles of the precomputed p×p D = (I − ZᵀZ)/ρ instead of Z; the adjoint contraction then IS b = D w
+// (u := w), the epilogue writes w⁺ straight to the next sweep's u buffer (double-buffered by sweep
+// parity) and there is no forward contraction and no cross-CTA reduction.
+//
 // Checks (every check_every iterations) use identities that need no pass over X:
 //   Xᵀr̂ = c − s,  ‖X b‖² = bᵀs   ⇒  dual(r̂ = y − Xb) = ½‖y‖² − ½ bᵀs − Σ ν_j(|c_j − s_j|)
 //   primal P(β) = ½‖y‖² − cᵀβ + ½‖Xβ‖² + Σ ψ_j(β_j)
