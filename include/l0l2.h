@@ -62,8 +62,10 @@ void l0l2_default_opts(l0l2_opts* o);
  *   c = Xᵀy, colsq_j = ‖X_j‖², A = XXᵀ + ρI_n = LLᵀ (Cholesky), Z = L⁻¹X (n×p).
  * D = (XᵀX+ρI)⁻¹ = (I − ZᵀZ)/ρ is then applied implicitly (Woodbury, P:375 with the 1/ρ²
  * typo corrected, R1).  X and y are copied (host or device per opts->x_on_device)
- * and never aliased afterwards.  Errors: L0L2_EINVAL (see above, and n > 1056: the ADMM kernel's
- * 3-stage tile ring of Z must fit one CTA's shared memory), L0L2_ENOMEM, L0L2_ECUDA.
+ * and never aliased afterwards.  For p ≤ 2n (and p ≤ 1056) the direct regime is used: D =
+ * (XᵀX + ρI)⁻¹ = (I − ZᵀZ)/ρ is precomputed (p×p) and the bound kernel streams D (R17).
+ * Errors: L0L2_EINVAL (see above, and n > 1056 outside the direct regime: the ADMM kernel's 3-stage
+ * tile ring of Z must fit one CTA's shared memory), L0L2_ENOMEM, L0L2_ECUDA.
  * On error *out is NULL.
  */
 int l0l2_create(const double* X, const double* y, int64_t n, int64_t p,

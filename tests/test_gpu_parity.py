@@ -473,3 +473,21 @@ def test_direct_regime_equals_zform(monkeypatch):
         r = O.admm_node(P, O.make_code(inst.p, *fx[k]), node_tol=1e-7, max_iters=3000)
         assert abs(float(la[k]) - r.lb) <= 1e-6 * max(1.0, abs(r.lb))
         assert int(a["iters"][k]) == r.iters
+
+
+def test_direct_regime_lifts_the_n_limit():
+    """n > 1056 with p ≤ min(2n, 1056): the direct regime streams D (p×p), so the Z-form's n limit
+    does not apply; fixed-iteration state vs the oracle."""
+    inst = synth.make_instance(1500, 300, 5, 0.3, 4.0, 8)
+    lam2 = 0.5
+    lam0, M = synth.lambda0_rule(inst, lam2), synth.bigM_rule(inst, lam2)
+    P = O.Problem(inst.X, inst.y, lam0, lam2, M)
+    prob = Problem(inst.X, inst.y, lam0, lam2, M, rho=P.rho, node_tol=-1.0, max_iters=29)
+    fx = _fixings(inst, 9, seed=3)
+    out = prob.l0l2_bound_batch(fx)
+    wo, lb = out["warm_out"].cpu().numpy(), out["lb"].cpu().numpy()
+    for k in (0, 4, 8):
+        r = O.admm_node(P, O.make_code(inst.p, *fx[k]), node_tol=-1.0, max_iters=29)
+        assert rel(wo[k, 0], r.beta) < 1e-9
+        assert abs(lb[k] - r.lb) <= 1e-9 * max(1.0, abs(r.lb))
+    prob.close()
