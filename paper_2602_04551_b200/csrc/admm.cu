@@ -930,7 +930,9 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     if (!k.direct) reduce_u(k, s, k.U);
     __shared__ int tot_s[kBC];
     if (chk) compact_nonzeros(k, s, tot_s);   // β⁺'s nonzeros → dense per-node lists
-    grid_sync(k.bar);
+    // (direct regime, no check: w⁺ is complete after the first barrier and the next sweep writes the
+    // other buffer, so one barrier per iteration suffices)
+    if (!k.direct || chk) grid_sync(k.bar);
     PROF_ACC(7);
     if (!chk) continue;
     PROF_RESET();
