@@ -377,7 +377,7 @@ __device__ void prefill(const KP& k, Smem& s, int sw, bool defer) {
 // iteration lives in registers as the adjoint's B fragments (MMA warp w owns k-steps [ks0, ks1),
 // lane holds U[row = 4q + lane%4][node = 8h + lane/4]).  Forward partials go to Upart[sub-range],
 // check sums to sums[sub-range], per sub-range (a paired CTA flushes at its sub-range boundary).
-template <int MODE, int KS, int MT>
+template <int MODE, int KS, int MT, bool DIR>
 __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& phases, unsigned& hph) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.x;
@@ -401,8 +401,8 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
   const int t0s = s.sched[6], t1s = s.sched[7];               // this sweep's tile range
   // direct regime (R17): this sweep reads w from uin and writes w⁺ to uout (double-buffered by
   // sweep parity; a CTA may finish its tiles while another still loads its u fragments)
-  const double* uin = (k.direct && (s.sched[0] & 1)) ? k.Ub : k.U;
-  double* uout = (k.direct && (s.sched[0] & 1)) ? k.U : k.Ub;
+  const double* uin = (DIR && (s.sched[0] & 1)) ? k.Ub : k.U;
+  double* uout = (DIR && (s.sched[0] & 1)) ? k.U : k.Ub;
   // wait for ring stage m; returns its tile (−1: the CTA's sweep is over)
   auto stage = [&](int m) {
     const int sg = m % NST;
@@ -481,7 +481,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       const int sg = m % NST;
       const bool nxt = fused ? adjoint(m + 1) : true;
       PROF_T0();
-      if (!flushed && ctile >= tb && !k.direct) { flush(sr0); flushed = true; }
+      if (!flushed && ctile >= tb && !DIR) { flush(sr0); flushed = true; }
       mbar_wait(&s.wready[m & 1], (hph >> (m & 1)) & 1u);   // w⁺_J(m) published
       hph ^= 1u << (m & 1);
       PROF_ACC(2);
@@ -493,7 +493,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       // two passes (k = cols 0-3, then 4-7), so consecutive DMMAs never share an accumulator (the
       // asm volatile DMMAs issue in source order; back-to-back dependent pairs stalled on latency)
 #ifndef EXP_NOFWD
-      if (!k.direct) {
+      if (!DIR) {
 #pragma unroll
         for (int i = 0; i < MT; i++) dmma(acc[i], T[8 * (warp + NMW * i)], b0);          // A[m = row][k = col j]
 #pragma unroll
@@ -520,7 +520,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       if (fused) { cur = nxt; ctile = ntile; }
       else { ctile = stage(m + 1); cur = ctile >= 0; }
     }
-    if (!k.direct) {
+    if (!DIR) {
       if (!flushed) flush(sr0);
       flush(paired ? sr0 + 1 : sr0);
     }
@@ -584,11 +584,11 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
         double bnz = 0.0;
         if (active) {
           // b = D w: Z-form D = (I − ZᵀZ)/ρ (R1) with sv = (ZᵀZ w)_j, or direct with sv = (D w)_j
-          const double b = k.direct ? sv : (w - sv) * k.inv_rho;
+          const double b = DIR ? sv : (w - sv) * k.inv_rho;
           const double bn = refresh ? q_beta : prox(k, b + vr, q_code);
           const double vn = q_v + k.rho * (b - bn);
           if (check) {
-            const double xxb = k.direct ? w - k.rho * b : sv;   // (XᵀX b)_j, since (XᵀX + ρI) b = w
+            const double xxb = DIR ? w - k.rho * b : sv;   // (XᵀX b)_j, since (XᵀX + ρI) b = w
             sT1 = fma(b, xxb, sT1);
             sT2 += nu_f(k, fabs(q_c - xxb), q_code);
             sT3 = fma(q_c, bn, sT3);
@@ -616,7 +616,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       }
 #endif
       s.Ws[(m & 1) * 8 * 12 + nd * 12 + j] = wn;
-      if (k.direct) uout[(int64_t)node * k.ld + col0 + j] = wn;   // the next sweep's w (R17)
+      if (DIR) uout[(int64_t)node * k.ld + col0 + j] = wn;   // the next sweep's w (R17)
       mbar_arrive_warp(&s.wready[m & 1]);
       PROF_ACC(5);
     }
@@ -866,7 +866,8 @@ __device__ void swap_slots(const KP& k, Smem& s, const int* pa, const int* pb, i
   grid_sync(k.bar);
 }
 
-template <int KS, int MT>
+// DIR: the direct regime (R17) as a separate instantiation, so the Z-form code is unchanged by it
+template <int KS, int MT, bool DIR>
 __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem s;
@@ -912,27 +913,27 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   __syncthreads();   // the sweep reads its node half and sub-ranges from s.sched
 
   // u0 = Z (c + ρβ0 − v0), then the warm/cold refresh sweep (R6)
-  sweep<SW_FWD_W, KS, MT>(k, s, false, false, phases, hph);
+  sweep<SW_FWD_W, KS, MT, DIR>(k, s, false, false, phases, hph);
   grid_sync(k.bar);
-  if (!k.direct) reduce_u(k, s, k.U);
+  if (!DIR) reduce_u(k, s, k.U);
   grid_sync(k.bar);
-  sweep<SW_FUSED, KS, MT>(k, s, true, false, phases, hph);
+  sweep<SW_FUSED, KS, MT, DIR>(k, s, true, false, phases, hph);
   grid_sync(k.bar);
-  if (!k.direct) reduce_u(k, s, k.U);
+  if (!DIR) reduce_u(k, s, k.U);
   grid_sync(k.bar);
 
   for (int it = 1; it <= k.max_iters; it++) {
     const bool chk = (it % k.check_every == 0) || (it == k.max_iters);
     PROF_T0();
-    sweep<SW_FUSED, KS, MT>(k, s, false, chk, phases, hph);
+    sweep<SW_FUSED, KS, MT, DIR>(k, s, false, chk, phases, hph);
     PROF_ACC(6);
     grid_sync(k.bar);
-    if (!k.direct) reduce_u(k, s, k.U);
+    if (!DIR) reduce_u(k, s, k.U);
     __shared__ int tot_s[kBC];
     if (chk) compact_nonzeros(k, s, tot_s);   // β⁺'s nonzeros → dense per-node lists
     // (direct regime, no check: w⁺ is complete after the first barrier and the next sweep writes the
     // other buffer, so one barrier per iteration suffices)
-    if (!k.direct || chk) grid_sync(k.bar);
+    if (!DIR || chk) grid_sync(k.bar);
     PROF_ACC(7);
     if (!chk) continue;
     PROF_RESET();
@@ -945,7 +946,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
       __syncthreads();
       for (int nd = 0; nd < kBC; nd++) dense |= (s.flags[nd] & F_ACTIVE) && tot_s[nd] > k.nz_cap;
       if (dense) {
-        sweep<SW_FWD_BETA, KS, MT>(k, s, false, false, phases, hph);
+        sweep<SW_FWD_BETA, KS, MT, DIR>(k, s, false, false, phases, hph);
         grid_sync(k.bar);
         reduce_u(k, s, k.Ub);
         grid_sync(k.bar);
@@ -1182,14 +1183,18 @@ __global__ void fill_y(double* r, int64_t ldr, const double* y, int64_t n, int n
 }
 
 using AdmmKernel = void (*)(KP);
-AdmmKernel admm_kernel(int cls) {
+template <bool DIR>
+AdmmKernel admm_kernel_t(int cls) {
   switch (cls) {
-    case 0: return admm_persistent<CLS_KS[0], CLS_MT[0]>;
-    case 1: return admm_persistent<CLS_KS[1], CLS_MT[1]>;
-    case 2: return admm_persistent<CLS_KS[2], CLS_MT[2]>;
-    case 3: return admm_persistent<CLS_KS[3], CLS_MT[3]>;
-    default: return admm_persistent<CLS_KS[4], CLS_MT[4]>;
+    case 0: return admm_persistent<CLS_KS[0], CLS_MT[0], DIR>;
+    case 1: return admm_persistent<CLS_KS[1], CLS_MT[1], DIR>;
+    case 2: return admm_persistent<CLS_KS[2], CLS_MT[2], DIR>;
+    case 3: return admm_persistent<CLS_KS[3], CLS_MT[3], DIR>;
+    default: return admm_persistent<CLS_KS[4], CLS_MT[4], DIR>;
   }
+}
+AdmmKernel admm_kernel(int cls, bool direct) {
+  return direct ? admm_kernel_t<true>(cls) : admm_kernel_t<false>(cls);
 }
 int admm_class(int64_t n8) {
   for (int c = 0; c < NCLS; c++)
@@ -1266,7 +1271,7 @@ int admm_alloc(Ctx* c) {
   L0L2_CUDA(c, cudaMemset(c->bchk, 0, sizeof(double) * p8 * kBC));
   L0L2_CUDA(c, cudaMemset(c->bar, 0, sizeof(unsigned) * 2));
   const size_t smem = admm_smem_bytes(ld);
-  const AdmmKernel kern = admm_kernel(c->admm_cls);
+  const AdmmKernel kern = admm_kernel(c->admm_cls, c->direct != 0);
   {
     // the 3-stage Z ring (24·ld doubles) must fit with everything else: n ≤ 1056 on B200
     int optin = 0;
@@ -1375,7 +1380,7 @@ int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
   k.psi_l1 = 2.0 * std::sqrt(c->lam0 * c->lam2);
   k.psi_4 = c->lam0 / c->M + c->lam2 * c->M;
   void* args[] = {&k};
-  L0L2_CUDA(c, cudaLaunchCooperativeKernel((void*)admm_kernel(c->admm_cls), dim3(c->grid), dim3(kAdmmThreads), args,
+  L0L2_CUDA(c, cudaLaunchCooperativeKernel((void*)admm_kernel(c->admm_cls, c->direct != 0), dim3(c->grid), dim3(kAdmmThreads), args,
                                            admm_smem_bytes(k.ld), st));
   L0L2_LAUNCHED(c);
   return L0L2_OK;
