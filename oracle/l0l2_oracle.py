@@ -33,7 +33,7 @@ __all__ = [
     "Problem", "make_code", "primal_value", "dual_value", "admm_node", "NodeResult",
     "box_ridge", "upper_bound", "brute_force", "relaxation_fista", "bnb_solve",
     "ub_objective", "default_rho", "MPResult", "mp_forward_scores", "mp_backward_scores",
-    "matching_pursuit",
+    "matching_pursuit", "finalize_node",
 ]
 
 
@@ -228,8 +228,10 @@ def admm_node(P: Problem, code, warm=None, parent_lb=-math.inf, node_tol=1e-4,
               check_every=10, max_iters=10000, int_tol=1e-4, prune_ub=math.inf) -> NodeResult:
     """ADMM on eq:ADMM1 for one node, warm start P:543.
 
-    Start: (β, v) = parent state or zeros; β_i ← 0 on F0; refresh b = D(c + ρβ − v),
-    v ← v + ρ(b − β) [R6: the cold start runs the same refresh from zeros].
+    Start ([R6]): a cold node (the root, or any node without a parent state) starts
+    from (β, v) = (0, 0) with no refresh ("For the root node, we initialize the ADMM variables
+    to zero").  A warm node takes the parent's (β, v), sets β_i ← 0 on F0, then refreshes
+    b = D(c + ρβ − v) (eq:b_update) and v ← v + ρ(b − β) (eq:v_i-update) before iterating.
     Iteration t: w = c + ρβ − v; b = D w (eq:b_update); β̃ = b + v/ρ (P:396);
     β = prox(β̃) (eq:minbetalower); v ← v + ρ(b − β) (eq:v_i-update).
     Every `check_every` iterations (and at max_iters): dual at r̂ = y − Xb,
@@ -244,14 +246,14 @@ def admm_node(P: Problem, code, warm=None, parent_lb=-math.inf, node_tol=1e-4,
     code = np.asarray(code, dtype=np.int8)
     p, rho = P.p, P.rho
     if warm is None:
-        beta = np.zeros(p)
+        beta = np.zeros(p)      # root / cold node: ADMM variables initialised to zero
         v = np.zeros(p)
     else:
         beta = np.array(warm[0], dtype=np.float64)
         v = np.array(warm[1], dtype=np.float64)
-    beta[code == FIX0] = 0.0
-    b = P.apply_D(P.c + rho * beta - v)
-    v = v + rho * (b - beta)
+        beta[code == FIX0] = 0.0                 # respect the new F0 fixings
+        b = P.apply_D(P.c + rho * beta - v)      # then update b (eq:b_update) ...
+        v = v + rho * (b - beta)                 # ... and v (eq:v_i-update)
     lb_best = -math.inf
     primal = math.inf
     duals = []
@@ -280,20 +282,36 @@ def admm_node(P: Problem, code, warm=None, parent_lb=-math.inf, node_tol=1e-4,
                 break
     kkt = max(float(np.max(np.abs(b - beta), initial=0.0)),
               rho * float(np.max(np.abs(beta - beta_prev), initial=0.0))) / (1.0 + float(np.max(np.abs(P.c), initial=0.0)))
-    z = recover_z(beta, code, P.lam0, P.lam2, P.M)
+    z, integral, support, branch_j = finalize_node(beta, code, P.lam0, P.lam2, P.M, int_tol)
+    return NodeResult(lb=max(lb_best, parent_lb), lb_best=lb_best, primal=primal, beta=beta, v=v, b=b,
+                      iters=it, converged=converged, z=z, integral=integral, support=support,
+                      branch_j=branch_j, kkt=kkt, duals=duals, pruned=pruned)
+
+
+def finalize_node(beta, code, lam0, lam2, M, int_tol=1e-4):
+    """Node finalize → (ẑ, integral, support, branch j).
+
+    ẑ = recover_z(β) (P:1088-1104); integral iff every free ẑ_i is within int_tol of {0, 1}
+    (S:224); support = F1 ∪ {free i: ẑ_i ≥ ½} (rounding, P:708, tie at ½ included [R13]);
+    branch j ("Select j ∈ [p] minus (F0 ∪ F1)") = the free coordinate with the largest
+    min(ẑ_j, 1 − ẑ_j), ties → larger |β_j|, then lower j [R10, S:381]; −1 when integral.
+    """
+    beta = np.asarray(beta, dtype=np.float64)
+    code = np.asarray(code, dtype=np.int8)
+    z = recover_z(beta, code, lam0, lam2, M)
     free = code == FREE
     frac = np.minimum(z, 1.0 - z)
     integral = bool(np.all(frac[free] <= int_tol))
     support = np.nonzero((code == FIX1) | (free & (z >= 0.5)))[0].astype(np.int64)
     branch_j = -1
     if not integral:
-        cand = np.nonzero(free)[0]
-        # lexsort: last key is primary → (−frac, −|β|, index)
-        order = np.lexsort((cand, -np.abs(beta[cand]), -frac[cand]))
-        branch_j = int(cand[order[0]])
-    return NodeResult(lb=max(lb_best, parent_lb), lb_best=lb_best, primal=primal, beta=beta, v=v, b=b,
-                      iters=it, converged=converged, z=z, integral=integral, support=support,
-                      branch_j=branch_j, kkt=kkt, duals=duals, pruned=pruned)
+        best = None
+        for j in np.nonzero(free)[0]:          # plain scan in index order: strict improvement only
+            key = (float(frac[j]), float(abs(beta[j])))
+            if best is None or key > best[0]:
+                best = (key, int(j))
+        branch_j = best[1]
+    return z, integral, support, branch_j
 
 
 # ----------------------------------------------------------------------------------------------

@@ -60,6 +60,29 @@ def test_golden_D_and_ub_and_mip(golden):
         assert res["obj"] == pytest.approx(e["obj"], abs=1e-12), e["cite"]
 
 
+def test_golden_admm_start(golden):
+    """the root (cold) node starts at β = v = 0 with NO refresh; a child takes the parent's
+    (β, v), zeroes β on F0, then refreshes b and v before iterating (hand-derived 1-D values)."""
+    for e in golden["admm_start"]:
+        P = O.Problem(np.array(e["X"]), np.array(e["y"]), e["lam0"], e["lam2"], e["M"], rho=e["rho"])
+        warm = None if e["warm"] is None else (np.array([e["warm"][0]]), np.array([e["warm"][1]]))
+        r = O.admm_node(P, np.array([CODES[e["code"]]], dtype=np.int8), warm=warm, node_tol=-1.0,
+                        max_iters=e["iters"])
+        assert r.beta[0] == pytest.approx(e["beta"], abs=1e-15), e["cite"]
+        assert r.v[0] == pytest.approx(e["v"], abs=1e-15), e["cite"]
+
+
+def test_golden_branch_rule(golden):
+    """R10: most fractional free ẑ, ties → larger |β_j|, then lower j; integrality
+     and the rounded support F1 ∪ {ẑ ≥ ½} on hand-built (β, code) vectors."""
+    for e in golden["branch"]:
+        code = np.array([CODES[c] for c in e["code"]], dtype=np.int8)
+        z, integral, support, j = O.finalize_node(np.array(e["beta"]), code, e["lam0"], e["lam2"], e["M"])
+        assert j == e["branch_j"], e["cite"]
+        assert integral == e["integral"], e["cite"]
+        assert list(support) == e["support"], e["cite"]
+
+
 # ---------------------------------------------------------------- operator properties
 def _rand_params(rng):
     lam0 = float(10 ** rng.uniform(-3, 1))
