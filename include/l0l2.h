@@ -51,7 +51,9 @@ typedef struct {
   int32_t check_every;  /* dual/primal check cadence in iterations; default 10          */
   int32_t max_iters;    /* ADMM iteration cap per node; default 10000                    */
   int32_t device;       /* CUDA device ordinal                                                   */
-  int32_t x_on_device;  /* 1: X, y passed to l0l2_create are device pointers on `device`        */
+  int32_t x_on_device;  /* 1: X, y passed to l0l2_create are device pointers on `device`; the
+                           library synchronises the device before copying them, so writes
+                           still pending on any stream complete first                          */
 } l0l2_opts;
 
 /* Fill `o` with the defaults above (M = 0 must then be set by the caller). */
@@ -168,6 +170,7 @@ typedef struct {
   double  lb, ub, gap;      /* certified global bounds at return                                 */
   int32_t status;           /* 0 optimal (queue exhausted), 1 gap reached, 2 node limit, 3 time limit */
   int32_t support_size;
+  int64_t nodes_moved;      /* open nodes moved between ranks by frontier rebalancing (Σ over ranks) */
 } l0l2_stats;
 
 /*
@@ -195,6 +198,25 @@ int64_t l0l2_solve_trace(const l0l2_ctx* ctx, double* rec, int64_t max_nodes);
  * broadcasts the id bytes).  NCCL is loaded at run time (libnccl.so.2).             */
 int l0l2_nccl_unique_id(uint8_t out[128]);
 int l0l2_comm_init(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id[128]);
+
+/* Alternative to NCCL: a caller-provided HOST transport (e.g. a gloo / MPI process group, or
+ * several ranks sharing one GPU, which NCCL rejects).  Every callback is collective in the usual
+ * sense, is called from the thread running l0l2_solve, moves HOST bytes, and returns 0 on success
+ * (anything else aborts the solve with L0L2_ENCCL):
+ *   allgather(user, in, out, bytes): out[r·bytes .. (r+1)·bytes) ← rank r's `in`, for every rank r
+ *   send(user, buf, bytes, peer) / recv(user, buf, bytes, peer): blocking point-to-point; every
+ *     send is matched by a recv of the same size issued by the peer in the same order
+ *   bcast(user, buf, bytes, root): buf ← root's buf on every rank
+ * The struct is copied; `user` must stay valid until l0l2_destroy.  Semantics of the exchange are
+ * those of the NCCL path; only the carrier differs. */
+typedef struct {
+  void* user;
+  int32_t (*allgather)(void* user, const void* in, void* out, int64_t bytes);
+  int32_t (*send)(void* user, const void* buf, int64_t bytes, int32_t peer);
+  int32_t (*recv)(void* user, void* buf, int64_t bytes, int32_t peer);
+  int32_t (*bcast)(void* user, void* buf, int64_t bytes, int32_t root);
+} l0l2_transport;
+int l0l2_comm_init_transport(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const l0l2_transport* t);
 
 /* Frontier rebalancing plan used by l0l2_solve every rebalance_every rounds (pure host logic,
  * exported for tests).  counts[r] = open nodes on rank r.  While the emptiest rank holds fewer

@@ -38,13 +38,22 @@ class _Stats(C.Structure):
                 ("nodes_global", C.c_int64), ("node_iters_global", C.c_int64),
                 ("t_total", C.c_double), ("t_bound", C.c_double), ("t_upper", C.c_double), ("t_tree", C.c_double),
                 ("t_comm", C.c_double), ("lb", C.c_double), ("ub", C.c_double), ("gap", C.c_double),
-                ("status", C.c_int32), ("support_size", C.c_int32)]
+                ("status", C.c_int32), ("support_size", C.c_int32), ("nodes_moved", C.c_int64)]
 
 
 class _KStats(C.Structure):
     _fields_ = [("admm_launches", C.c_int64), ("admm_iters", C.c_int64), ("admm_node_iters", C.c_int64),
                 ("admm_ms", C.c_double), ("admm_bytes_alg", C.c_double), ("admm_flops_alg", C.c_double),
                 ("upper_launches", C.c_int64), ("upper_ms", C.c_double), ("upper_bytes_alg", C.c_double)]
+
+
+_ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64)
+_P2P_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32)
+
+
+class _Transport(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allgather", _ALLGATHER_FN), ("send", _P2P_FN), ("recv", _P2P_FN),
+                ("bcast", _P2P_FN)]
 
 
 _lib = None
@@ -84,6 +93,8 @@ def load_library():
     lib.l0l2_nccl_unique_id.restype = C.c_int
     lib.l0l2_comm_init.argtypes = [P, C.c_int32, C.c_int32, P]
     lib.l0l2_comm_init.restype = C.c_int
+    lib.l0l2_comm_init_transport.argtypes = [P, C.c_int32, C.c_int32, C.POINTER(_Transport)]
+    lib.l0l2_comm_init_transport.restype = C.c_int
     lib.l0l2_rebalance_plan.argtypes = [C.c_int32, P, C.c_int64, P, C.c_int32]
     lib.l0l2_rebalance_plan.restype = C.c_int
     lib.l0l2_kernel_stats.argtypes = [P, C.POINTER(_KStats), C.c_int32]
@@ -132,6 +143,57 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+class HostTransport:
+    """l0l2_transport callbacks over a torch.distributed process group (e.g. gloo): host bytes in,
+    host bytes out — marshalling only; the exchange logic lives in the library (solve.cu)."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        W = dist.get_world_size(group)
+
+        def view(addr, nbytes):
+            return torch.from_numpy(np.ctypeslib.as_array((C.c_uint8 * int(nbytes)).from_address(addr)))
+
+        def allgather(user, inp, out, nbytes):
+            try:
+                outs = [torch.empty(int(nbytes), dtype=torch.uint8) for _ in range(W)]
+                dist.all_gather(outs, view(inp, nbytes).clone(), group=group)
+                view(out, W * nbytes).copy_(torch.cat(outs))
+                return 0
+            except Exception:
+                return 1
+
+        def send(user, buf, nbytes, peer):
+            try:
+                dist.send(view(buf, nbytes).clone(), dst=int(peer), group=group)
+                return 0
+            except Exception:
+                return 1
+
+        def recv(user, buf, nbytes, peer):
+            try:
+                t = torch.empty(int(nbytes), dtype=torch.uint8)
+                dist.recv(t, src=int(peer), group=group)
+                view(buf, nbytes).copy_(t)
+                return 0
+            except Exception:
+                return 1
+
+        def bcast(user, buf, nbytes, root):
+            try:
+                t = view(buf, nbytes).clone()
+                dist.broadcast(t, src=int(root), group=group)
+                view(buf, nbytes).copy_(t)
+                return 0
+            except Exception:
+                return 1
+
+        self._fns = (_ALLGATHER_FN(allgather), _P2P_FN(send), _P2P_FN(recv), _P2P_FN(bcast))
+        self.struct = _Transport(None, *self._fns)
+
+
 def _ptr(t):
     """Device pointer of a torch CUDA tensor (or None → NULL)."""
     if t is None:
@@ -168,6 +230,7 @@ class Problem:
             if not X.T.is_contiguous():
                 X = X.T.contiguous().T
             yv = y.contiguous()
+            torch.cuda.current_stream(X.device).synchronize()   # X, y complete before the library copies them
             o.x_on_device = 1
             xp, yp = X.data_ptr(), yv.data_ptr()
             self._keep += [X, yv]
@@ -289,10 +352,20 @@ class Problem:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         _check(self._lib.l0l2_comm_init(self._ctx, int(nranks), int(rank), C.cast(buf, P)), self._ctx)
 
-    def init_distributed(self):
-        """Build the NCCL communicator from the current torch.distributed process group."""
+    def l0l2_comm_init_transport(self, nranks, rank, transport: HostTransport):
+        self._transport = transport   # the callbacks must outlive the context
+        _check(self._lib.l0l2_comm_init_transport(self._ctx, int(nranks), int(rank), C.byref(transport.struct)),
+               self._ctx)
+
+    def init_distributed(self, transport="nccl"):
+        """Attach the current torch.distributed process group: transport "nccl" builds an NCCL
+        communicator (one GPU per rank); "host" routes the same exchange through HostTransport
+        callbacks on the group (gloo; also several ranks sharing one GPU)."""
         import torch.distributed as dist
         if not dist.is_initialized() or dist.get_world_size() == 1:
+            return
+        if transport == "host":
+            self.l0l2_comm_init_transport(dist.get_world_size(), dist.get_rank(), HostTransport())
             return
         obj = [nccl_unique_id() if dist.get_rank() == 0 else None]
         dist.broadcast_object_list(obj, src=0)

@@ -49,6 +49,7 @@ constexpr int NEW = 2;                  // epilogue warps
 constexpr int NH = kBC / 8;             // node halves (one per CTA of a pair)
 static_assert(NH == 2, "a CTA pair serves the two node halves");
 constexpr int F_ACTIVE = 64;            // internal node flag bit (not exported)
+constexpr int F_COLD = 128;             // internal: cold node (β = v = 0, no warm refresh)
 
 struct KP {
   const double* __restrict__ Z;
@@ -378,7 +379,8 @@ __device__ void prefill(const KP& k, Smem& s, int sw, bool defer) {
 // lane holds U[row = 4q + lane%4][node = 8h + lane/4]).  Forward partials go to Upart[sub-range],
 // check sums to sums[sub-range], per sub-range (a paired CTA flushes at its sub-range boundary).
 template <int MODE, int KS, int MT, bool DIR>
-__device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& phases, unsigned& hph) {
+__device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& phases, unsigned& hph,
+                      double* sums_out = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.x;
   constexpr bool fused = (MODE == SW_FUSED);
@@ -528,6 +530,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
     // ---------------- epilogue warps: element (j = et>>3, node = 8h + (et&7)) of each 8×8 block
     const int et = tid - MMA_THREADS, j = et >> 3, nd = et & 7, node = 8 * h + nd;
     const bool active = (s.flags[node] & F_ACTIVE) != 0;
+    const bool cold = (s.flags[node] & F_COLD) != 0;
     double sT1 = 0.0, sT2 = 0.0, sT3 = 0.0, sT4 = 0.0;
     const int ew = et >> 5;   // epilogue warp: columns 4·ew .. 4·ew + 3 of each tile
     int seg_n = 0;            // β⁺ nonzeros of (sub-range, warp ew, node) so far (check sweeps)
@@ -586,7 +589,8 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
           // b = D w: Z-form D = (I − ZᵀZ)/ρ (R1) with sv = (ZᵀZ w)_j, or direct with sv = (D w)_j
           const double b = DIR ? sv : (w - sv) * k.inv_rho;
           const double bn = refresh ? q_beta : prox(k, b + vr, q_code);
-          const double vn = q_v + k.rho * (b - bn);
+          // the refresh sweep updates b, v of warm nodes only; a cold node starts at (0, 0) (R6)
+          const double vn = (refresh && cold) ? q_v : q_v + k.rho * (b - bn);
           if (check) {
             const double xxb = DIR ? w - k.rho * b : sv;   // (XᵀX b)_j, since (XᵀX + ρI) b = w
             sT1 = fma(b, xxb, sT1);
@@ -639,7 +643,7 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
     const int si = tid >> 5, nd = (tid >> 2) & 7, q = tid & 3;
     double a = 0.0;
     for (int j = 0; j < 8; j++) a += s.Ws[2 * 8 * 12 + (si * 64 + j * 8 + nd) * 4 + q];
-    k.sums[((int64_t)(sr0 + si) * kBC + 8 * h + nd) * kSums + q] = a;
+    sums_out[((int64_t)(sr0 + si) * kBC + 8 * h + nd) * kSums + q] = a;
   }
 }
 
@@ -912,7 +916,8 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   if (tid == 0) prefill(k, s, 0, false);
   __syncthreads();   // the sweep reads its node half and sub-ranges from s.sched
 
-  // u0 = Z (c + ρβ0 − v0), then the warm/cold refresh sweep (R6)
+  // u0 = Z (c + ρβ0 − v0), then the warm-start refresh sweep (R6: b, v of warm nodes; cold
+  // nodes keep β = v = 0 and only their w⁺ = c is formed)
   sweep<SW_FWD_W, KS, MT, DIR>(k, s, false, false, phases, hph);
   grid_sync(k.bar);
   if (!DIR) reduce_u(k, s, k.U);
@@ -922,10 +927,15 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   if (!DIR) reduce_u(k, s, k.U);
   grid_sync(k.bar);
 
+  int nchk = 0;   // checks so far: the per-sub-range check sums are double-buffered by its parity, so a
+                 // CTA that runs ahead into the next check sweep (no grid barrier follows a decision)
+                 // never overwrites the sums a slower CTA is still reading in its decision step
   for (int it = 1; it <= k.max_iters; it++) {
     const bool chk = (it % k.check_every == 0) || (it == k.max_iters);
+    double* sums_cur = k.sums + (size_t)(nchk & 1) * k.nsr * kBC * kSums;
+    if (chk) nchk++;
     PROF_T0();
-    sweep<SW_FUSED, KS, MT, DIR>(k, s, false, chk, phases, hph);
+    sweep<SW_FUSED, KS, MT, DIR>(k, s, false, chk, phases, hph, sums_cur);
     PROF_ACC(6);
     grid_sync(k.bar);
     if (!DIR) reduce_u(k, s, k.U);
@@ -969,7 +979,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
           const int q0 = Q * ch / RCH, q1 = Q * (ch + 1) / RCH;
 #pragma unroll 8
           for (int q = q0; q < q1; q++)
-            a += term < 4 ? __ldcg(k.sums + ((int64_t)q * kBC + nd) * kSums + term)
+            a += term < 4 ? __ldcg(sums_cur + ((int64_t)q * kBC + nd) * kSums + term)
                           : __ldcg(k.sums2 + (int64_t)q * kBC + nd);
         }
         cs[tid] = a;
@@ -1079,14 +1089,14 @@ __global__ void scatter_fix(int nb, const int64_t* __restrict__ off, const int32
   }
 }
 
-__global__ void init_nodes(int nb, unsigned mask, const double* parent_lb, double* nodef, int* nodei) {
+__global__ void init_nodes(int nb, unsigned mask, unsigned cold, const double* parent_lb, double* nodef, int* nodei) {
   const int nd = threadIdx.x;
   if (nd >= kBC) return;
   nodef[nd * 4 + 0] = -INFINITY;
   nodef[nd * 4 + 1] = INFINITY;
   nodef[nd * 4 + 2] = (nd < nb && parent_lb) ? parent_lb[nd] : -INFINITY;
   nodef[nd * 4 + 3] = -INFINITY;
-  nodei[nd * 2 + 0] = (nd < nb && ((mask >> nd) & 1u)) ? F_ACTIVE : 0;
+  nodei[nd * 2 + 0] = (nd < nb && ((mask >> nd) & 1u)) ? (F_ACTIVE | (((cold >> nd) & 1u) ? F_COLD : 0)) : 0;
   nodei[nd * 2 + 1] = 0;
 }
 
@@ -1244,7 +1254,7 @@ int admm_alloc(Ctx* c) {
   c->U = (double*)dalloc(c, sizeof(double) * kBC * ld);
   c->Ub = (double*)dalloc(c, sizeof(double) * kBC * ld);
   c->Upart = (double*)dalloc(c, sizeof(double) * c->grid * kBC * ld);
-  c->sums = (double*)dalloc(c, sizeof(double) * c->grid * kBC * kSums);
+  c->sums = (double*)dalloc(c, sizeof(double) * 2 * c->grid * kBC * kSums);   // double-buffered by check parity
   c->sums2 = (double*)dalloc(c, sizeof(double) * c->grid * kBC);
   // sparse primal check: per-CTA segments of β⁺'s nonzeros (capacity = the CTA's columns) and the
   // dense per-node lists (capacity p/16: above it the forward-only Zβ sweep is cheaper)
@@ -1337,7 +1347,7 @@ int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st) {
 }
 
 int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
-  init_nodes<<<1, 32, 0, st>>>(a.nb, mask, a.parent_lb, c->node_f, c->node_i);
+  init_nodes<<<1, 32, 0, st>>>(a.nb, mask, a.cold_mask, a.parent_lb, c->node_f, c->node_i);
   L0L2_LAUNCHED(c);
   KP k{};
   k.act_mask = mask;
@@ -1354,7 +1364,9 @@ int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
   k.nodef = c->node_f; k.nodei = c->node_i; k.bar = c->bar;
   k.seg_idx = c->seg_idx; k.seg_val = c->seg_val; k.seg_cnt = c->seg_cnt; k.nz_idx = c->nz_idx; k.nz_val = c->nz_val;
   k.X = c->X; k.seg_cap = c->seg_cap; k.nz_cap = c->nz_cap;
-  if (const char* e = getenv("L0L2_NZCAP")) k.nz_cap = std::min(k.nz_cap, atoi(e));   // testing hook (0 = always sweep)
+  // testing hook (0 = always the dense sweep); the direct regime has no dense fallback (it needs Z)
+  if (const char* e = getenv("L0L2_NZCAP"))
+    if (!c->direct) k.nz_cap = std::min(k.nz_cap, atoi(e));
   k.out_lb = a.lb; k.out_primal = a.primal; k.out_iters = a.iters; k.out_flags = a.flags;
   k.ld = c->direct ? c->ldD : c->ld;
   k.n = c->direct ? c->p : c->n;

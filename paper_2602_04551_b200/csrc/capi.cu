@@ -149,6 +149,9 @@ int l0l2_create(const double* X, const double* y, int64_t n, int64_t p, double l
             ck(cudaMemsetAsync(c->c, 0, sizeof(double) * p8, st), "memset c") &&
             ck(cudaMemsetAsync(c->colsq, 0, sizeof(double) * p8, st), "memset colsq");
   const cudaMemcpyKind kind = opts->x_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  // device-resident X, y may still be being written on a caller's stream that has no ordering with
+  // this library's non-blocking stream: wait for all prior device work before copying them
+  if (opts->x_on_device) ok = ok && ck(cudaDeviceSynchronize(), "synchronize before copying device X, y");
   ok = ok && ck(cudaMemcpy2DAsync(c->X, sizeof(double) * ld, X, sizeof(double) * n, sizeof(double) * n, p, kind, st),
                 "copy X") &&
        ck(cudaMemcpyAsync(c->y, y, sizeof(double) * n, kind, st), "copy y");
@@ -231,6 +234,7 @@ int l0l2_bound_batch(l0l2_ctx* ctx, int32_t B, const int64_t* fix_off, const int
     int rc = pack_group(c, nb, fix_off ? fix_off + g0 : nullptr, fix_idx, fix_val, (const double* const*)wptr, st);
     if (rc) return rc;
     BoundArgs a{nb, parent_lb ? parent_lb + g0 : nullptr, lb + g0, primal + g0, iters + g0, flags + g0};
+    for (int k = 0; k < nb; k++) if (!hin[k]) a.cold_mask |= 1u << k;
     rc = run_admm(c, a, st);
     if (rc) return rc;
     rc = finalize_group(c, nb, zhat ? zhat + (int64_t)g0 * p : nullptr, branch_j + g0, flags + g0, scnt, sidx, p, st);

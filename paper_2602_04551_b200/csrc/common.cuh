@@ -99,6 +99,9 @@ struct Ctx {
   void* nccl_comm = nullptr;
   NcclApi* nccl = nullptr;
   cudaStream_t comm_stream = nullptr;
+  // caller-provided host transport (l0l2_comm_init_transport): used instead of NCCL when set
+  l0l2_transport host_tr{};
+  bool host_tr_set = false;
   // kept across l0l2_solve calls (allocation and stream creation are not free): the warm-state
   // pool chunks, the round I/O block (sized for solve_buf_B nodes), the solve stream, the pool cap
   std::vector<double*> pool_chunks;
@@ -146,6 +149,7 @@ struct BoundArgs {
   int *iters;                   // device [nb]
   uint8_t* flags;               // device [nb]
   double prune_ub = INFINITY;   // stop a node once its best dual reaches this (early prune, R16)
+  unsigned cold_mask = 0;       // nodes without a parent state: start at β = v = 0, no refresh (R6)
 };
 int pack_group(Ctx* c, int nb, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
                const double* const* warm_ptrs_dev, cudaStream_t st);

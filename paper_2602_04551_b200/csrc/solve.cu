@@ -158,7 +158,9 @@ struct RoundBufs {
 };
 
 struct Status {   // exchanged every round (8 doubles = 64 B per rank)
-  double ub, lbmin, open, nodes, iters, elapsed, sent, pad;
+  // ub: the rank's pruning threshold (its own incumbent or an adopted global UB); own: the objective
+  // of the incumbent VECTOR this rank holds (never an adopted value), which elects the owner of β*
+  double ub, lbmin, open, nodes, iters, elapsed, own, pad;
 };
 
 // Deterministic rebalancing plan from the open counts of all ranks (pure host logic):
@@ -196,7 +198,8 @@ struct Solver {
   SlotPool pool;
   RoundBufs d;
   std::priority_queue<Node, std::vector<Node>, NodeCmp> open;
-  double UB = 0.0;
+  double UB = 0.0;                 // pruning threshold (≤ inc_ub: may be a global UB adopted from a peer)
+  double inc_ub = 0.0;             // objective of the incumbent vector (inc_S, inc_b) held by this rank
   std::vector<int32_t> inc_S;
   std::vector<double> inc_b;
   int64_t next_id = 1, nodes = 0, node_iters = 0, rounds = 0, max_open = 0;
@@ -208,6 +211,7 @@ struct Solver {
   bool partitioned = false;
   int64_t id_counter = 0, id_base = 0;
   int ub_owner = 0;
+  int64_t moved = 0;   // nodes this rank sent away by rebalancing
 
   int64_t new_id() {
     if (!partitioned) return next_id++;
@@ -303,6 +307,7 @@ struct Solver {
       int rc = pack_group(c, nb, d.fix_off + g0, dfi, dfv, (const double* const*)d.wptr, st);
       if (rc) return rc;
       BoundArgs a{nb, d.parent_lb + g0, d.lb + g0, d.primal + g0, d.iters + g0, d.flags + g0};
+      for (int k = 0; k < nb; k++) if (!hp[k]) a.cold_mask |= 1u << k;
       if (o.early_prune) a.prune_ub = UB * (1.0 - 1e-12);   // UB of the round's start (R16)
       if ((rc = run_admm(c, a, st))) return rc;
       if ((rc = finalize_group(c, nb, nullptr, d.branch + g0, d.flags + g0, d.scnt + g0, d.sidx, p, st))) return rc;
@@ -378,10 +383,9 @@ struct Solver {
     std::sort(order.begin(), order.end(), [&](int a, int b) { return batch[a].id < batch[b].id; });
     for (int k : order)
       if (res[k].obj < UB) {
-        UB = res[k].obj;
+        UB = inc_ub = res[k].obj;
         inc_S = res[k].supp;
         inc_b = res[k].beta_s;
-        ub_owner = R;
       }
     if (trace)
       for (int k : order) {
@@ -428,36 +432,119 @@ struct Solver {
 
   double local_lbmin() const { return open.empty() ? INFINITY : open.top().lb; }
 
-  // ---- multi-rank helpers
-  int allgather_status(const Status& mine, std::vector<Status>& all) {
-    auto t0 = Clock::now();
-    double* dbuf = (double*)c->scratch_n(2, sizeof(double) * 8 * (W + 1));
-    if (!dbuf) return set_err(c, L0L2_ENOMEM, "status buffer");
-    L0L2_CUDA(c, cudaMemcpyAsync(dbuf, &mine, sizeof(Status), cudaMemcpyHostToDevice, st));
-    NCCL_CK(c, c->nccl->AllGather(dbuf, dbuf + 8, 8, ncclFloat64, (ncclComm_t)c->nccl_comm, st));
-    all.resize(W);
-    L0L2_CUDA(c, cudaMemcpyAsync(all.data(), dbuf + 8, sizeof(Status) * W, cudaMemcpyDeviceToHost, st));
+  // ---- multi-rank helpers.  The carrier is NCCL (device buffers on the solve stream) or the
+  // caller's host transport (l0l2_comm_init_transport); the exchange logic is the same.
+  bool host_tr() const { return c->host_tr_set; }
+  int tr_fail(const char* what) { return set_err(c, L0L2_ENCCL, "host transport %s failed", what); }
+
+  // all-gather `bytes` of host data from every rank into out[W·bytes]
+  int xg_allgather(const void* in, void* out, size_t bytes) {
+    if (host_tr()) {
+      const l0l2_transport& t = c->host_tr;
+      return t.allgather(t.user, in, out, (int64_t)bytes) ? tr_fail("allgather") : L0L2_OK;
+    }
+    char* dbuf = (char*)c->scratch_n(2, bytes * (W + 1));
+    if (!dbuf) return set_err(c, L0L2_ENOMEM, "allgather buffer");
+    L0L2_CUDA(c, cudaMemcpyAsync(dbuf, in, bytes, cudaMemcpyHostToDevice, st));
+    NCCL_CK(c, c->nccl->AllGather(dbuf, dbuf + bytes, bytes, ncclChar, (ncclComm_t)c->nccl_comm, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(out, dbuf + bytes, bytes * W, cudaMemcpyDeviceToHost, st));
     L0L2_CUDA(c, cudaStreamSynchronize(st));
-    t_comm += secs(t0);
+    return L0L2_OK;
+  }
+  // point-to-point of DEVICE bytes (send on src, recv on dst, same order on both)
+  int xg_send_dev(const void* d, size_t bytes, int peer) {
+    if (host_tr()) {
+      std::vector<char> h(bytes);
+      L0L2_CUDA(c, cudaMemcpyAsync(h.data(), d, bytes, cudaMemcpyDeviceToHost, st));
+      L0L2_CUDA(c, cudaStreamSynchronize(st));
+      const l0l2_transport& t = c->host_tr;
+      return t.send(t.user, h.data(), (int64_t)bytes, peer) ? tr_fail("send") : L0L2_OK;
+    }
+    NCCL_CK(c, c->nccl->Send(d, bytes, ncclChar, peer, (ncclComm_t)c->nccl_comm, st));
+    return L0L2_OK;
+  }
+  int xg_recv_dev(void* d, size_t bytes, int peer) {
+    if (host_tr()) {
+      std::vector<char> h(bytes);
+      const l0l2_transport& t = c->host_tr;
+      if (t.recv(t.user, h.data(), (int64_t)bytes, peer)) return tr_fail("recv");
+      L0L2_CUDA(c, cudaMemcpyAsync(d, h.data(), bytes, cudaMemcpyHostToDevice, st));
+      L0L2_CUDA(c, cudaStreamSynchronize(st));
+      return L0L2_OK;
+    }
+    NCCL_CK(c, c->nccl->Recv(d, bytes, ncclChar, peer, (ncclComm_t)c->nccl_comm, st));
+    return L0L2_OK;
+  }
+  // host bytes point-to-point (staged through the device for NCCL)
+  int xg_send_host(const void* h, size_t bytes, int peer) {
+    if (host_tr()) {
+      const l0l2_transport& t = c->host_tr;
+      return t.send(t.user, h, (int64_t)bytes, peer) ? tr_fail("send") : L0L2_OK;
+    }
+    char* d = (char*)c->scratch_n(2, std::max<size_t>(8, bytes));
+    if (!d) return set_err(c, L0L2_ENOMEM, "send buffer");
+    L0L2_CUDA(c, cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+    int rc = xg_send_dev(d, bytes, peer);
+    if (rc) return rc;
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    return L0L2_OK;
+  }
+  int xg_recv_host(void* h, size_t bytes, int peer) {
+    if (host_tr()) {
+      const l0l2_transport& t = c->host_tr;
+      return t.recv(t.user, h, (int64_t)bytes, peer) ? tr_fail("recv") : L0L2_OK;
+    }
+    char* d = (char*)c->scratch_n(2, std::max<size_t>(8, bytes));
+    if (!d) return set_err(c, L0L2_ENOMEM, "recv buffer");
+    int rc = xg_recv_dev(d, bytes, peer);
+    if (rc) return rc;
+    L0L2_CUDA(c, cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    return L0L2_OK;
+  }
+  int xg_bcast_host(void* h, size_t bytes, int root) {
+    if (host_tr()) {
+      const l0l2_transport& t = c->host_tr;
+      return t.bcast(t.user, h, (int64_t)bytes, root) ? tr_fail("bcast") : L0L2_OK;
+    }
+    char* d = (char*)c->scratch_n(3, std::max<size_t>(8, bytes));
+    if (!d) return set_err(c, L0L2_ENOMEM, "bcast buffer");
+    L0L2_CUDA(c, cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+    NCCL_CK(c, c->nccl->Broadcast(d, d, bytes, ncclChar, root, (ncclComm_t)c->nccl_comm, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
     return L0L2_OK;
   }
 
-  // send k nodes (odd positions of the local best-first order first) from src to dst
+  int allgather_status(const Status& mine, std::vector<Status>& all) {
+    auto t0 = Clock::now();
+    all.resize(W);
+    int rc = xg_allgather(&mine, all.data(), sizeof(Status));
+    t_comm += secs(t0);
+    return rc;
+  }
+
+  // Move k nodes (the odd positions of the local best-first order first, then from the tail) from
+  // src to dst with their warm states.  The source sends a header with the number of nodes it
+  // actually holds for the move (≤ k), then per node [lb, id, depth, nfix, has_warm], then the
+  // fixings and the warm states; the destination allocates pool slots (cold start when the pool is
+  // full: the bound stays valid, only the warm start is lost).
   int rebalance(const std::vector<int64_t>& plan) {
     auto t0 = Clock::now();
     const int64_t p = c->p;
     for (size_t q = 0; q + 2 < plan.size(); q += 3) {
       const int src = (int)plan[q], dst = (int)plan[q + 1];
-      const int64_t k = plan[q + 2];
+      int64_t k = plan[q + 2];
       if (R != src && R != dst) continue;
       const int peer = (R == src) ? dst : src;
-      // meta: per node [lb, id, depth, nfix, has_warm]
-      std::vector<double> meta(5 * k, 0.0);
-      std::vector<int32_t> fix;
       std::vector<Node> out;
+      int64_t hdr[2] = {0, 0};   // nodes moved, fixings moved
+      std::vector<double> meta;
+      std::vector<int32_t> fix;
       if (R == src) {
         std::vector<Node> all;
         while (!open.empty()) { all.push_back(open.top()); open.pop(); }
+        k = std::min<int64_t>(k, (int64_t)all.size());
         std::vector<Node> keep;
         for (size_t i = 0; i < all.size(); i++) {
           if ((int64_t)out.size() < k && (i % 2 == 1 || (int64_t)(all.size() - i) <= k - (int64_t)out.size()))
@@ -466,7 +553,8 @@ struct Solver {
             keep.push_back(std::move(all[i]));
         }
         for (auto& u : keep) open.push(std::move(u));
-        for (int64_t i = 0; i < k; i++) {
+        meta.assign(5 * out.size(), 0.0);
+        for (size_t i = 0; i < out.size(); i++) {
           const Node& u = out[i];
           meta[5 * i + 0] = u.lb;
           meta[5 * i + 1] = (double)u.id;
@@ -475,61 +563,57 @@ struct Solver {
           meta[5 * i + 4] = u.slot >= 0 ? 1.0 : 0.0;
           for (size_t f = 0; f < u.fidx.size(); f++) fix.push_back(u.fidx[f] * 2 + u.fval[f]);
         }
-      }
-      double* dmeta = (double*)c->scratch_n(2, sizeof(double) * std::max<int64_t>(8, 5 * k));
-      if (!dmeta) return set_err(c, L0L2_ENOMEM, "rebalance buffers");
-      if (R == src) L0L2_CUDA(c, cudaMemcpyAsync(dmeta, meta.data(), sizeof(double) * 5 * k, cudaMemcpyHostToDevice, st));
-      NCCL_CK(c, c->nccl->GroupStart());
-      if (R == src) NCCL_CK(c, c->nccl->Send(dmeta, 5 * k, ncclFloat64, peer, (ncclComm_t)c->nccl_comm, st));
-      else NCCL_CK(c, c->nccl->Recv(dmeta, 5 * k, ncclFloat64, peer, (ncclComm_t)c->nccl_comm, st));
-      NCCL_CK(c, c->nccl->GroupEnd());
-      if (R == dst) {
-        L0L2_CUDA(c, cudaMemcpyAsync(meta.data(), dmeta, sizeof(double) * 5 * k, cudaMemcpyDeviceToHost, st));
-        L0L2_CUDA(c, cudaStreamSynchronize(st));
-      }
-      int64_t nfix = 0;
-      for (int64_t i = 0; i < k; i++) nfix += (int64_t)meta[5 * i + 3];
-      // fixings and warm states in one device buffer: [nfix int32 padded to doubles][k × 2p]
-      const int64_t fix_d = (nfix + 1) / 2;
-      double* dpay = (double*)c->scratch_n(3, sizeof(double) * std::max<int64_t>(1, fix_d + k * 2 * p));
-      if (!dpay) return set_err(c, L0L2_ENOMEM, "rebalance payload");
-      if (R == src) {
-        if (nfix) L0L2_CUDA(c, cudaMemcpyAsync(dpay, fix.data(), sizeof(int32_t) * nfix, cudaMemcpyHostToDevice, st));
-        for (int64_t i = 0; i < k; i++) {
-          double* dstp = dpay + fix_d + i * 2 * p;
-          if (out[i].slot >= 0)
-            L0L2_CUDA(c, cudaMemcpyAsync(dstp, pool.ptr(out[i].slot), sizeof(double) * 2 * p, cudaMemcpyDeviceToDevice, st));
-          else
-            L0L2_CUDA(c, cudaMemsetAsync(dstp, 0, sizeof(double) * 2 * p, st));
+        hdr[0] = (int64_t)out.size();
+        hdr[1] = (int64_t)fix.size();
+        int rc = xg_send_host(hdr, sizeof(hdr), peer);
+        if (!rc && hdr[0]) rc = xg_send_host(meta.data(), sizeof(double) * meta.size(), peer);
+        if (!rc && hdr[1]) rc = xg_send_host(fix.data(), sizeof(int32_t) * fix.size(), peer);
+        if (rc) return rc;
+        // warm states: one device payload of hdr[0] × 2p doubles
+        if (hdr[0]) {
+          double* dpay = (double*)c->scratch_n(3, sizeof(double) * hdr[0] * 2 * p);
+          if (!dpay) return set_err(c, L0L2_ENOMEM, "rebalance payload");
+          for (int64_t i = 0; i < hdr[0]; i++) {
+            double* dstp = dpay + i * 2 * p;
+            if (out[i].slot >= 0)
+              L0L2_CUDA(c, cudaMemcpyAsync(dstp, pool.ptr(out[i].slot), sizeof(double) * 2 * p, cudaMemcpyDeviceToDevice, st));
+            else
+              L0L2_CUDA(c, cudaMemsetAsync(dstp, 0, sizeof(double) * 2 * p, st));
+          }
+          if ((rc = xg_send_dev(dpay, sizeof(double) * hdr[0] * 2 * p, peer))) return rc;
+          L0L2_CUDA(c, cudaStreamSynchronize(st));
         }
-      }
-      NCCL_CK(c, c->nccl->GroupStart());
-      if (R == src) NCCL_CK(c, c->nccl->Send(dpay, fix_d + k * 2 * p, ncclFloat64, peer, (ncclComm_t)c->nccl_comm, st));
-      else NCCL_CK(c, c->nccl->Recv(dpay, fix_d + k * 2 * p, ncclFloat64, peer, (ncclComm_t)c->nccl_comm, st));
-      NCCL_CK(c, c->nccl->GroupEnd());
-      if (R == src) {
-        L0L2_CUDA(c, cudaStreamSynchronize(st));
         for (auto& u : out) pool.release(u.slot);
+        moved += hdr[0];
       } else {
-        std::vector<int32_t> hf(nfix);
-        if (nfix) L0L2_CUDA(c, cudaMemcpyAsync(hf.data(), dpay, sizeof(int32_t) * nfix, cudaMemcpyDeviceToHost, st));
-        L0L2_CUDA(c, cudaStreamSynchronize(st));
+        int rc = xg_recv_host(hdr, sizeof(hdr), peer);
+        if (rc) return rc;
+        meta.assign(5 * hdr[0], 0.0);
+        fix.assign(hdr[1], 0);
+        if (hdr[0] && (rc = xg_recv_host(meta.data(), sizeof(double) * meta.size(), peer))) return rc;
+        if (hdr[1] && (rc = xg_recv_host(fix.data(), sizeof(int32_t) * fix.size(), peer))) return rc;
+        double* dpay = nullptr;
+        if (hdr[0]) {
+          dpay = (double*)c->scratch_n(3, sizeof(double) * hdr[0] * 2 * p);
+          if (!dpay) return set_err(c, L0L2_ENOMEM, "rebalance payload");
+          if ((rc = xg_recv_dev(dpay, sizeof(double) * hdr[0] * 2 * p, peer))) return rc;
+        }
         int64_t f = 0;
-        for (int64_t i = 0; i < k; i++) {
+        for (int64_t i = 0; i < hdr[0]; i++) {
           Node u;
           u.lb = meta[5 * i + 0];
           u.id = (int64_t)meta[5 * i + 1];
           u.depth = (int32_t)meta[5 * i + 2];
           const int64_t nf = (int64_t)meta[5 * i + 3];
           for (int64_t q2 = 0; q2 < nf; q2++, f++) {
-            u.fidx.push_back(hf[f] >> 1);
-            u.fval.push_back((uint8_t)(hf[f] & 1));
+            u.fidx.push_back(fix[f] >> 1);
+            u.fval.push_back((uint8_t)(fix[f] & 1));
           }
           u.slot = -1;
           if (meta[5 * i + 4] != 0.0) {
             u.slot = pool.alloc();
             if (u.slot >= 0)
-              L0L2_CUDA(c, cudaMemcpyAsync(pool.ptr(u.slot), dpay + fix_d + i * 2 * p, sizeof(double) * 2 * p,
+              L0L2_CUDA(c, cudaMemcpyAsync(pool.ptr(u.slot), dpay + i * 2 * p, sizeof(double) * 2 * p,
                                            cudaMemcpyDeviceToDevice, st));
           }
           open.push(std::move(u));
@@ -603,8 +687,21 @@ int l0l2_comm_init(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id
   ncclComm_t comm;
   NCCL_CK(c, c->nccl->CommInitRank(&comm, nranks, uid, rank));
   c->nccl_comm = comm;
+  c->host_tr_set = false;
   c->nranks = nranks;
   c->rank = rank;
+  return L0L2_OK;
+}
+
+int l0l2_comm_init_transport(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const l0l2_transport* t) {
+  if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) return L0L2_EINVAL;
+  Ctx* c = &ctx->impl;
+  if (nranks > 1 && (!t || !t->allgather || !t->send || !t->recv || !t->bcast))
+    return set_err(c, L0L2_EINVAL, "transport callbacks missing");
+  c->nranks = nranks;
+  c->rank = rank;
+  c->host_tr_set = nranks > 1;
+  if (t) c->host_tr = *t;
   return L0L2_OK;
 }
 
@@ -640,7 +737,7 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
   S.o = o;
   S.W = c->nranks;
   S.R = c->rank;
-  if (S.W > 1 && !c->nccl_comm) return set_err(c, L0L2_ENCCL, "communicator not initialised");
+  if (S.W > 1 && !c->nccl_comm && !c->host_tr_set) return set_err(c, L0L2_ENCCL, "communicator not initialised");
   if (!c->solve_stream) L0L2_CUDA(c, cudaStreamCreateWithFlags(&c->solve_stream, cudaStreamNonBlocking));
   S.st = c->solve_stream;
   struct StreamGuard { cudaStream_t s; ~StreamGuard() { if (s) cudaStreamSynchronize(s); } } sg{S.st};
@@ -661,7 +758,7 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
   if (o.record) S.trace = &c->trace;
   int rc = S.alloc_bufs(o.batch);
   if (rc) return rc;
-  S.UB = 0.5 * c->yy;   // β = 0 is feasible
+  S.UB = S.inc_ub = 0.5 * c->yy;   // β = 0 is feasible
   if (o.init_mp) {
     // root heuristic (Algorithm 3): MP's own point, then the box ridge on its support
     auto t0 = Clock::now();
@@ -670,7 +767,7 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
     double mobj = 0.0;
     if ((rc = mp_run(c, 0, S.st, mS, mb, &mobj, nullptr))) return rc;
     if (mobj < S.UB) {
-      S.UB = mobj;
+      S.UB = S.inc_ub = mobj;
       S.inc_S = mS;
       S.inc_b.assign(mS.size(), 0.0);
       for (size_t i = 0; i < mS.size(); i++) S.inc_b[i] = mb[mS[i]];
@@ -688,7 +785,7 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
       L0L2_CUDA(c, cudaMemcpyAsync(h.data(), dres, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, S.st));
       L0L2_CUDA(c, cudaStreamSynchronize(S.st));
       if (h[0] < S.UB) {
-        S.UB = h[0];
+        S.UB = S.inc_ub = h[0];
         S.inc_S = mS;
         S.inc_b.assign(h.begin() + 1, h.end());
       }
@@ -707,24 +804,26 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
     int64_t gopen = (int64_t)S.open.size(), gnodes = S.nodes;
     double elapsed = secs(T0);
     if (S.W > 1) {
-      Status mine{S.UB, S.local_lbmin(), (double)S.open.size(), (double)S.nodes, (double)S.node_iters, elapsed, 0, 0};
+      Status mine{S.UB, S.local_lbmin(), (double)S.open.size(), (double)S.nodes, (double)S.node_iters, elapsed,
+                  S.inc_ub, 0};
       if ((rc = S.allgather_status(mine, all))) return rc;
       gopen = 0;
       gnodes = 0;
       gLB = INFINITY;
-      int owner = 0;
       for (int r = 0; r < S.W; r++) {
-        if (all[r].ub < gUB || (all[r].ub == gUB && r < owner)) { gUB = all[r].ub; owner = r; }
+        gUB = std::min(gUB, all[r].ub);
         gLB = std::min(gLB, all[r].lbmin);
         gopen += (int64_t)all[r].open;
         gnodes += (int64_t)all[r].nodes;
         elapsed = std::max(elapsed, all[r].elapsed);
       }
-      // owner = lowest rank holding the global UB
-      for (int r = 0; r < S.W; r++) if (all[r].ub == gUB) { owner = r; break; }
-      S.ub_owner = owner;
+      // owner of β* = the lowest rank whose OWN incumbent vector attains the global UB (a rank that
+      // only adopted the value holds no matching vector)
+      int owner = -1;
+      for (int r = 0; r < S.W && owner < 0; r++) if (all[r].own == gUB) owner = r;
+      S.ub_owner = owner < 0 ? 0 : owner;
       if (gUB < S.UB) {
-        S.UB = gUB;   // incumbent vector stays with its owner until the end
+        S.UB = gUB;   // the incumbent vector stays with its owner until the end
         S.prune_open();
       }
     } else {
@@ -737,10 +836,16 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
     if (o.time_limit_s > 0 && elapsed >= o.time_limit_s) { status = 3; break; }
     if (S.W > 1) {
       if (!S.partitioned) {
-        if (gopen >= S.W) S.partition();   // every rank holds the same tree until here
+        // every rank holds the same tree until here (identical rounds): split it once the LOCAL
+        // frontier has a node for every rank
+        if ((int64_t)S.open.size() >= S.W) S.partition();
       } else if (o.rebalance_every > 0 && S.rounds % o.rebalance_every == 0) {
+        // the plan needs the open counts AFTER the global-UB prune above: exchange them
+        const int64_t mine_open = (int64_t)S.open.size();
         std::vector<int64_t> cnt(S.W);
-        for (int r = 0; r < S.W; r++) cnt[r] = (int64_t)all[r].open;
+        auto t0 = Clock::now();
+        if ((rc = S.xg_allgather(&mine_open, cnt.data(), sizeof(int64_t)))) return rc;
+        S.t_comm += secs(t0);
         std::vector<int64_t> plan = rebalance_plan(cnt, o.batch);
         if (!plan.empty() && (rc = S.rebalance(plan))) return rc;
       }
@@ -764,18 +869,15 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
   const int64_t p = c->p;
   std::vector<double> hb(p, 0.0);
   for (size_t i = 0; i < S.inc_S.size(); i++) hb[S.inc_S[i]] = S.inc_b[i];
-  double final_ub = S.UB;
+  double final_ub = S.inc_ub;
   if (S.W > 1) {
+    // the owner (elected at the last status exchange, after which no rank solved a node) sends its
+    // incumbent vector and that vector's own objective
     auto t0 = Clock::now();
-    double* db = (double*)c->scratch_n(3, sizeof(double) * (p + 1));
-    if (!db) return set_err(c, L0L2_ENOMEM, "beta buffer");
-    hb.push_back(S.UB);
-    L0L2_CUDA(c, cudaMemcpyAsync(db, hb.data(), sizeof(double) * (p + 1), cudaMemcpyHostToDevice, S.st));
-    NCCL_CK(c, c->nccl->Broadcast(db, db, p + 1, ncclFloat64, S.ub_owner, (ncclComm_t)c->nccl_comm, S.st));
-    L0L2_CUDA(c, cudaMemcpyAsync(hb.data(), db, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost, S.st));
-    L0L2_CUDA(c, cudaStreamSynchronize(S.st));
+    hb.push_back(S.inc_ub);
+    if ((rc = S.xg_bcast_host(hb.data(), sizeof(double) * (p + 1), S.ub_owner))) return rc;
     final_ub = hb[p];
-    Status mine{S.UB, 0, 0, (double)S.nodes, (double)S.node_iters, 0, 0, 0};
+    Status mine{S.UB, 0, 0, (double)S.nodes, (double)S.node_iters, 0, S.inc_ub, (double)S.moved};
     if ((rc = S.allgather_status(mine, all))) return rc;
     S.t_comm += secs(t0);
   }
@@ -791,7 +893,10 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
     stats->max_open = S.max_open;
     stats->nodes_global = S.nodes;
     stats->node_iters_global = S.node_iters;
+    stats->nodes_moved = S.moved;
     if (S.W > 1) {
+      stats->nodes_moved = 0;
+      for (int r = 0; r < S.W; r++) stats->nodes_moved += (int64_t)all[r].pad;
       stats->nodes_global = 0;
       stats->node_iters_global = 0;
       for (int r = 0; r < S.W; r++) {

@@ -75,3 +75,46 @@ def test_status_exchange_and_rebalance_agree_across_ranks(world):
         assert len(res) == 20
         for same, conserved, not_worse in res:
             assert same and conserved and not_worse
+
+
+def _transport_worker(rank, world, port, q):
+    """The HostTransport callbacks (the marshalling the library calls during a multi-rank solve),
+    invoked through their C function pointers exactly as solve.cu invokes them."""
+    import ctypes as C
+    import numpy as np
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2602_04551_b200 import HostTransport
+    t = HostTransport().struct
+    ok = []
+    mine = np.array([rank + 0.5, -rank, 7.0 * rank], dtype=np.float64)
+    out = np.zeros(3 * world)
+    ok.append(t.allgather(None, mine.ctypes.data, out.ctypes.data, mine.nbytes) == 0)
+    ok.append(np.array_equal(out, np.concatenate([[r + 0.5, -r, 7.0 * r] for r in range(world)])))
+    buf = np.arange(5, dtype=np.int64) * (rank + 1)
+    ok.append(t.bcast(None, buf.ctypes.data, buf.nbytes, 1) == 0)
+    ok.append(np.array_equal(buf, np.arange(5) * 2))
+    pay = np.full(4, 3.25) if rank == 0 else np.zeros(4)
+    if rank == 0:
+        ok.append(t.send(None, pay.ctypes.data, pay.nbytes, 1) == 0)
+    else:
+        ok.append(t.recv(None, pay.ctypes.data, pay.nbytes, 0) == 0)
+        ok.append(np.array_equal(pay, np.full(4, 3.25)))
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, all(ok)))
+
+
+def test_host_transport_callbacks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_transport_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in out), out
