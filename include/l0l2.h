@@ -239,7 +239,9 @@ typedef struct {
 } l0l2_kstats;
 int l0l2_kernel_stats(l0l2_ctx* ctx, l0l2_kstats* out, int32_t reset);
 
-/* Introspection: n, p, ρ actually used, device bytes held, and kernel launches so far. */
+/* Introspection: n, p, ρ actually used, device bytes held by the context (problem data, ADMM work
+ * space, batch scratch, solve buffers, warm-state pool; all kept until l0l2_destroy, so this is
+ * also the peak), and kernel launches so far. */
 int l0l2_info(const l0l2_ctx* ctx, int64_t* n, int64_t* p, double* rho, int64_t* device_bytes,
               int64_t* kernel_launches);
 

@@ -452,9 +452,18 @@ def relaxation_fista(P: Problem, code, tol=1e-12, max_iters=200000):
 # Branch-and-bound: batched reading of Algorithm 1
 # ----------------------------------------------------------------------------------------------
 
+def _solve_node(args):
+    """One node of a BnB round: its relaxation (admm_node) and the UB on its rounded support."""
+    P, code, warm, plb, node_tol, check_every, max_iters, int_tol, prune_ub = args
+    res = admm_node(P, code, warm=warm, parent_lb=plb, node_tol=node_tol, check_every=check_every,
+                    max_iters=max_iters, int_tol=int_tol, prune_ub=prune_ub)
+    obj, bS = upper_bound(P, res.support)
+    return res, obj, bS
+
+
 def bnb_solve(P: Problem, B=1, gap_tol=1e-2, node_tol=1e-4, check_every=10, max_iters=10000,
               int_tol=1e-4, prune_tol=1e-12, node_limit=None, time_limit=None, record=False,
-              early_prune=False):
+              early_prune=False, init_mp=False, node_map=map):
     """Best-first synchronous-round BnB (Algorithm 1) [R9, R11].
 
     UB starts at ½‖y‖² (β = 0 is feasible).  Each round: drop open nodes with
@@ -467,11 +476,25 @@ def bnb_solve(P: Problem, B=1, gap_tol=1e-2, node_tol=1e-4, check_every=10, max_
     early_prune [R16]: each node's ADMM stops at the first check whose LB_best ≥ UB(1−prune_tol)
     with UB the incumbent at the start of the round (the node is then pruned by the rule above,
     since the round can only lower UB).
+    node_map: how the round's independent node solves are mapped (default the builtin map, one
+    after the other; a multiprocessing pool's map runs them on several cores — the nodes of a round
+    are independent, so the tree is identical).
+    init_mp (P:781-783, "we use ... matching pursuit ... to obtain an initial upper bound"): before
+    the root, the incumbent is the better of β = 0, Algorithm 3's own point (matching_pursuit) and
+    the exact box ridge on its support (upper_bound), strict improvements only, in that order.
     """
     t0 = time.perf_counter()
     p = P.p
     UB = 0.5 * P.yy
     inc_S, inc_b = np.zeros(0, dtype=np.int64), np.zeros(0)
+    if init_mp:
+        mp = matching_pursuit(P)
+        if mp.obj < UB:
+            UB, inc_S, inc_b = mp.obj, mp.support, mp.beta[mp.support]
+        if len(mp.support):
+            obj, bS = upper_bound(P, mp.support)
+            if obj < UB:
+                UB, inc_S, inc_b = obj, mp.support, bS
     # open node: (lb, id, depth, F0 tuple, F1 tuple, warm)
     open_nodes = [(-math.inf, 0, 0, (), (), None)]
     next_id = 1
@@ -499,12 +522,10 @@ def bnb_solve(P: Problem, B=1, gap_tol=1e-2, node_tol=1e-4, check_every=10, max_
         rounds += 1
         results = []
         prune_ub = UB * (1 - prune_tol) if early_prune else math.inf
-        for (plb, uid, depth, F0, F1, warm) in batch:
-            code = make_code(p, F0, F1)
-            res = admm_node(P, code, warm=warm, parent_lb=plb, node_tol=node_tol,
-                            check_every=check_every, max_iters=max_iters, int_tol=int_tol,
-                            prune_ub=prune_ub)
-            obj, bS = upper_bound(P, res.support)
+        jobs = [(make_code(p, F0, F1), warm, plb) for (plb, uid, depth, F0, F1, warm) in batch]
+        solved = list(node_map(_solve_node, [(P, code, warm, plb, node_tol, check_every, max_iters, int_tol,
+                                               prune_ub) for (code, warm, plb) in jobs]))
+        for (plb, uid, depth, F0, F1, warm), (res, obj, bS) in zip(batch, solved):
             results.append((uid, depth, F0, F1, res, obj, bS))
             nodes += 1
             node_iters += res.iters

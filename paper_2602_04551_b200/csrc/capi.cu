@@ -197,7 +197,16 @@ int l0l2_info(const l0l2_ctx* ctx, int64_t* n, int64_t* p, double* rho, int64_t*
   if (n) *n = c->n;
   if (p) *p = c->p;
   if (rho) *rho = c->rho;
-  if (device_bytes) *device_bytes = c->bytes;
+  if (device_bytes) {
+    // everything the context holds on the device: problem data and ADMM work space, the growable
+    // batch I/O scratch, the solve's round buffers and the warm-state pool chunks (all kept until
+    // l0l2_destroy, so this is also the peak)
+    int64_t b = c->bytes;
+    for (size_t s : c->scr_bytes) b += (int64_t)s;
+    b += (int64_t)c->solve_buf_bytes;
+    b += (int64_t)c->pool_chunks.size() * c->pool_chunk_bytes;
+    *device_bytes = b;
+  }
   if (launches) *launches = c->launches;
   return L0L2_OK;
 }

@@ -106,6 +106,8 @@ struct Ctx {
   // pool chunks, the round I/O block (sized for solve_buf_B nodes), the solve stream, the pool cap
   std::vector<double*> pool_chunks;
   void* solve_buf = nullptr;
+  size_t solve_buf_bytes = 0;
+  int64_t pool_chunk_bytes = 0;   // bytes per warm-pool chunk (2p doubles × slots per chunk)
   int solve_buf_B = 0;
   cudaStream_t solve_stream = nullptr;
   size_t pool_cap = 0;

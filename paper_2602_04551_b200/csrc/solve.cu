@@ -130,6 +130,7 @@ struct SlotPool {
         return -1;
       }
       chunk().push_back(m);
+      c->pool_chunk_bytes = (int64_t)(sizeof(double) * 2 * p * kPerChunk);
       add_slots();
     }
     const int s = freel.back();
@@ -235,6 +236,7 @@ struct Solver {
         return set_err(c, L0L2_ENOMEM, "solve buffers");
       }
       c->solve_buf_B = Bmax;
+      c->solve_buf_bytes = need;
     }
     char* cur = (char*)c->solve_buf;
     auto A = [&](size_t b) { void* r = cur; cur += (b + 255) / 256 * 256; return r; };
