@@ -243,6 +243,7 @@ struct Smem {
   unsigned* rel;      // [NST] MMA warps done with the stage (last one refills it)
   int* ncnt;          // [kBC]            per-node β⁺ nonzero totals at a check (lmatvec fallback)
   int* stile;         // [NST]            tile held by each ring slot (−1: end of this CTA's sweep)
+  int* zres;          // [NST]            tile whose Z_J is in the slot (−1: none yet)
   int* sched;         // [9]              sweep number, stages issued, tiles taken, done (issuer
                       //                  only); node half, paired, tile range [t0, t1) of the sweep,
                       //                  issue deferred
@@ -279,15 +280,22 @@ __shared__ unsigned long long prof_s[NW][8];
 __device__ __forceinline__ unsigned tile_bytes(const KP& k) { return (unsigned)(kPt * k.ld * sizeof(double)); }
 
 // stage t → ring slot sg: Z_J plus the epilogue operands of the same columns (one mbarrier)
+// Resident tiles: a slot keeps the Z_J it last received (zres[slot] = its tile), so when a CTA's tiles
+// of a sweep fit the ring (≤ NST tiles, e.g. C2's 125 tiles of D on ≥ 124 CTAs) every later sweep
+// re-stages only the tile's state block — Z_J stays in shared memory for the whole launch.
 __device__ __forceinline__ void issue_stage(const KP& k, Smem& s, int t, int sg) {
   const unsigned tb = tile_bytes(k);
-  mbar_expect_tx(&s.mbar[sg], tb + STQ_BYTES);
+  const bool have = s.zres[sg] == t;
+  mbar_expect_tx(&s.mbar[sg], (have ? 0u : tb) + STQ_BYTES);
   // Z_J as k.tsplit bulk copies of kPt/tsplit whole columns each (1 is fastest: every copy issued
   // costs the issuing MMA warp time on the critical path)
   const int cpc = kPt / k.tsplit;
-  for (int c = 0; c < kPt; c += cpc)
-    bulk_g2s(s.tiles + (size_t)sg * kPt * k.ld + c * k.ld, k.Z + ((int64_t)t * kPt + c) * k.ld,
-             (unsigned)(cpc * k.ld * sizeof(double)), &s.mbar[sg]);
+  if (!have) {
+    s.zres[sg] = t;
+    for (int c = 0; c < kPt; c += cpc)
+      bulk_g2s(s.tiles + (size_t)sg * kPt * k.ld + c * k.ld, k.Z + ((int64_t)t * kPt + c) * k.ld,
+               (unsigned)(cpc * k.ld * sizeof(double)), &s.mbar[sg]);
+  }
   // the tile's whole state block (β_J, v_J, c_J, code_J) in one copy
   bulk_g2s(s.stq + sg * STQ, k.stt + (int64_t)t * STQ, STQ_BYTES, &s.mbar[sg]);
 }
@@ -889,7 +897,8 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     s.rel = reinterpret_cast<unsigned*>(s.flags + kBC);
     s.ncnt = reinterpret_cast<int*>(s.rel + NST);
     s.stile = s.ncnt + kBC;
-    s.sched = s.stile + NST;
+    s.zres = s.stile + NST;
+    s.sched = s.zres + NST;
   }
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -900,7 +909,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < NST) s.rel[tid] = 0;
+  if (tid < NST) { s.rel[tid] = 0; s.zres[tid] = -1; }
   for (size_t i = tid; i < (size_t)NST * kPt * k.ld + NST * STQ; i += blockDim.x) s.tiles[i] = 0.0;   // stq follows
   if (tid < kBC) {
     s.flags[tid] = __ldcg(k.nodei + tid * 2);
@@ -1229,7 +1238,7 @@ int debug_prof(unsigned long long*, int) { return 0; }
 
 size_t admm_smem_bytes(int64_t ld) {
   return sizeof(double) * ((size_t)NST * kPt * ld + NST * STQ + 2 * NMW * 64 + 2 * 8 * 12 + 2 * 64 * 4 + kBC) +
-         (NST + 4) * sizeof(uint64_t) + 2 * kBC * sizeof(int) + (NST + 12) * sizeof(int) + NST * sizeof(unsigned) + 64;
+         (NST + 4) * sizeof(uint64_t) + 2 * kBC * sizeof(int) + (2 * NST + 12) * sizeof(int) + NST * sizeof(unsigned) + 64;
 }
 
 int admm_alloc(Ctx* c) {
@@ -1246,6 +1255,9 @@ int admm_alloc(Ctx* c) {
   // barrier / reduction cost (C2, 125 tiles: ADMM 13% faster on 64 CTAs than on 124; C4 unchanged)
   // (two tiles per sub-range at most: ⌈ntiles/2⌉ sub-ranges, rounded up to even)
   c->grid = std::min(c->sms, std::max(2, ((ntiles + 1) / 2 + 1) & ~1));
+  // ≤ 1 tile per sub-range (a paired CTA then streams ≤ 2 tiles, fewer than the ring's NST slots):
+  // the tiles stay resident in shared memory across the sweeps of a launch (issue_stage)
+  if (ntiles <= c->sms) c->grid = std::min(c->sms, std::max(2, (ntiles + 1) & ~1));
   if (const char* e = getenv("L0L2_GRID")) c->grid = std::max(1, std::min(c->grid, atoi(e)));   // testing hook
   c->grid = std::max(2, c->grid & ~1);
   c->stt = (double*)dalloc(c, sizeof(double) * (p8 / kPt) * STQ);
