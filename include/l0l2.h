@@ -155,6 +155,13 @@ typedef struct {
   int32_t early_prune;      /* 1: a node's ADMM stops at the first check whose best dual ≥ UB(1−1e-12),
                                UB = the incumbent at the start of its round (the node is pruned
                                anyway; R16); 0 (default): run to node_tol        */
+  int32_t continuous;       /* continuous batching (P:272 reads the batch as a
+                               snapshot): k > 0 → when at most k nodes of a 16-node launch are still
+                               iterating (at a regular check, after ≥ 2·check_every iterations) while
+                               open nodes wait, the launch suspends them; they resume bitwise where
+                               they stopped in the next launch, next to fresh nodes.  Bounds and the
+                               certificate are unchanged; the tree order (node ids) differs from the
+                               synchronous rounds.  Single rank only.  0 (default): synchronous      */
 } l0l2_solve_opts;
 
 void l0l2_default_solve_opts(l0l2_solve_opts* o);
@@ -171,6 +178,7 @@ typedef struct {
   int32_t status;           /* 0 optimal (queue exhausted), 1 gap reached, 2 node limit, 3 time limit */
   int32_t support_size;
   int64_t nodes_moved;      /* open nodes moved between ranks by frontier rebalancing (Σ over ranks) */
+  int64_t suspensions;      /* continuous batching: node suspensions (each node resumed later)       */
 } l0l2_stats;
 
 /*
@@ -189,8 +197,10 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts, double* beta, double*
                l0l2_stats* stats);
 
 /* Per-node trace of the last l0l2_solve run with opts.record = 1 (this rank's nodes, in the
- * order they were solved).  Record r occupies rec[8r .. 8r+7] =
- *   {node id, depth, LB, primal P(β), ADMM iterations, branch j (−1 = none), flags, UB on its support}.
+ * order they were solved; suspended launches of a node are not records, its finishing one is).
+ * Record r occupies rec[10r .. 10r+9] =
+ *   {node id, depth, LB, primal P(β), ADMM iterations, branch j (−1 = none), flags, UB on its support,
+ *    parent id (−1 = root), fixing that created it: 2j + value (value 0 → F0, 1 → F1; −1 = root)}.
  * Returns the number of records available (may exceed max_nodes; only max_nodes are written). */
 int64_t l0l2_solve_trace(const l0l2_ctx* ctx, double* rec, int64_t max_nodes);
 

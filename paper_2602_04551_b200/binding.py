@@ -30,7 +30,7 @@ class _SolveOpts(C.Structure):
     _fields_ = [("gap_tol", C.c_double), ("time_limit_s", C.c_double), ("node_limit", C.c_int64),
                 ("batch", C.c_int32), ("rebalance_every", C.c_int32), ("warm_bytes_cap", C.c_int64),
                 ("verbose", C.c_int32), ("record", C.c_int32), ("init_mp", C.c_int32),
-                ("early_prune", C.c_int32)]
+                ("early_prune", C.c_int32), ("continuous", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -38,7 +38,8 @@ class _Stats(C.Structure):
                 ("nodes_global", C.c_int64), ("node_iters_global", C.c_int64),
                 ("t_total", C.c_double), ("t_bound", C.c_double), ("t_upper", C.c_double), ("t_tree", C.c_double),
                 ("t_comm", C.c_double), ("lb", C.c_double), ("ub", C.c_double), ("gap", C.c_double),
-                ("status", C.c_int32), ("support_size", C.c_int32), ("nodes_moved", C.c_int64)]
+                ("status", C.c_int32), ("support_size", C.c_int32), ("nodes_moved", C.c_int64),
+                ("suspensions", C.c_int64)]
 
 
 class _KStats(C.Structure):
@@ -372,7 +373,7 @@ class Problem:
         self.l0l2_comm_init(dist.get_world_size(), dist.get_rank(), obj[0])
 
     def l0l2_solve(self, gap_tol=1e-2, batch=16, time_limit_s=0.0, node_limit=0, rebalance_every=8,
-                   warm_bytes_cap=0, verbose=False, record=False, init_mp=False, early_prune=False):
+                   warm_bytes_cap=0, verbose=False, record=False, init_mp=False, early_prune=False, continuous=0):
         so = _SolveOpts()
         self._lib.l0l2_default_solve_opts(C.byref(so))
         so.gap_tol, so.batch, so.time_limit_s = float(gap_tol), int(batch), float(time_limit_s)
@@ -381,6 +382,7 @@ class Problem:
         so.record = int(bool(record))
         so.init_mp = int(bool(init_mp))
         so.early_prune = int(bool(early_prune))
+        so.continuous = int(continuous)
         beta = np.zeros(self.p, dtype=np.float64)
         obj, gap = C.c_double(), C.c_double()
         st = _Stats()
@@ -390,8 +392,9 @@ class Problem:
         out = dict(beta=beta, obj=obj.value, gap=gap.value, support=np.nonzero(beta)[0], stats=stats, rc=rc)
         if record:
             nrec = self._lib.l0l2_solve_trace(self._ctx, None, 0)
-            buf = np.zeros((max(1, nrec), 8))
+            buf = np.zeros((max(1, nrec), 10))
             self._lib.l0l2_solve_trace(self._ctx, buf.ctypes.data, nrec)
             out["trace"] = [dict(id=int(r[0]), depth=int(r[1]), lb=r[2], primal=r[3], iters=int(r[4]),
-                                 branch_j=int(r[5]), flags=int(r[6]), ub=r[7]) for r in buf[:nrec]]
+                                 branch_j=int(r[5]), flags=int(r[6]), ub=r[7], parent=int(r[8]), lastfix=int(r[9]))
+                            for r in buf[:nrec]]
         return out

@@ -49,7 +49,9 @@ constexpr int NEW = 2;                  // epilogue warps
 constexpr int NH = kBC / 8;             // node halves (one per CTA of a pair)
 static_assert(NH == 2, "a CTA pair serves the two node halves");
 constexpr int F_ACTIVE = 64;            // internal node flag bit (not exported)
-constexpr int F_COLD = 128;             // internal: cold node (β = v = 0, no warm refresh)
+constexpr int F_COLD = 128;             // internal: cold node (β = v = 0, no warm refresh) or a
+                                        // resumed (suspended) node: its state continues, no refresh
+constexpr int F_SUSP = 32;              // internal: suspended at a check (continuous batching, §8(f) rank 2)
 
 struct KP {
   const double* __restrict__ Z;
@@ -73,6 +75,10 @@ struct KP {
   int ntiles, nsr, nb, check_every, max_iters, pfd;   // nsr: tile sub-ranges (= grid)
   unsigned act_mask;               // node slots run by this launch (outputs written for these only)
   double prune_ub;                 // early prune threshold (R16; +inf = off)
+  int suspend_at;                  // continuous batching: at a check with ≤ suspend_at active nodes (and
+                                   // ≥ susp_min iterations in this launch) the launch suspends them (0 = off)
+  int susp_min;
+  double* out_lbbest;              // [nb] running max of checked duals (to resume a suspended node), or null
   int compact;                     // node-slot compaction allowed (tuning / test hook)
   int pfs;                         // tiles L2-prefetched by prefill (during the grid reduction)
   int tsplit;                      // bulk copies per Z tile (divides kPt)
@@ -244,6 +250,7 @@ struct Smem {
   int* ncnt;          // [kBC]            per-node β⁺ nonzero totals at a check (lmatvec fallback)
   int* stile;         // [NST]            tile held by each ring slot (−1: end of this CTA's sweep)
   int* zres;          // [NST]            tile whose Z_J is in the slot (−1: none yet)
+  int* it0;           // [kBC]            iterations a (resumed) node had run before this launch
   int* sched;         // [9]              sweep number, stages issued, tiles taken, done (issuer
                       //                  only); node half, paired, tile range [t0, t1) of the sweep,
                       //                  issue deferred
@@ -845,6 +852,7 @@ __device__ void swap_slots(const KP& k, Smem& s, const int* pa, const int* pb, i
     for (int q = 0; q < np; q++) {
       const int a = pa[q], b = pb[q];
       int f = s.flags[a]; s.flags[a] = s.flags[b]; s.flags[b] = f;
+      f = s.it0[a]; s.it0[a] = s.it0[b]; s.it0[b] = f;
       double r = s.red[a]; s.red[a] = s.red[b]; s.red[b] = r;
       if (g == 0) {
         for (int i = 0; i < 4; i++) { double t = k.nodef[a * 4 + i]; k.nodef[a * 4 + i] = k.nodef[b * 4 + i]; k.nodef[b * 4 + i] = t; }
@@ -898,7 +906,8 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     s.ncnt = reinterpret_cast<int*>(s.rel + NST);
     s.stile = s.ncnt + kBC;
     s.zres = s.stile + NST;
-    s.sched = s.zres + NST;
+    s.it0 = s.zres + NST;
+    s.sched = s.it0 + kBC;
   }
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -913,7 +922,8 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
   for (size_t i = tid; i < (size_t)NST * kPt * k.ld + NST * STQ; i += blockDim.x) s.tiles[i] = 0.0;   // stq follows
   if (tid < kBC) {
     s.flags[tid] = __ldcg(k.nodei + tid * 2);
-    s.red[tid] = -INFINITY;
+    s.it0[tid] = __ldcg(k.nodei + tid * 2 + 1);   // 0, or the iterations of a resumed node
+    s.red[tid] = __ldcg(k.nodef + tid * 4);       // −∞, or the best dual of a resumed node (R7)
   }
   __syncthreads();
 #ifdef L0L2_PROF
@@ -940,7 +950,9 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
                  // CTA that runs ahead into the next check sweep (no grid barrier follows a decision)
                  // never overwrites the sums a slower CTA is still reading in its decision step
   for (int it = 1; it <= k.max_iters; it++) {
-    const bool chk = (it % k.check_every == 0) || (it == k.max_iters);
+    bool chk = (it % k.check_every == 0) || (it == k.max_iters);
+    for (int nd = 0; nd < kBC; nd++)   // a resumed node reaching its own iteration cap
+      chk |= (s.flags[nd] & F_ACTIVE) && s.it0[nd] + it == k.max_iters;
     double* sums_cur = k.sums + (size_t)(nchk & 1) * k.nsr * kBC * kSums;
     if (chk) nchk++;
     PROF_T0();
@@ -1012,14 +1024,14 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
         bool conv = (primal - lbb) / fmax(1.0, fabs(primal)) <= k.node_tol;
         if (conv) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_CONVERGED;
         else if (lbb >= k.prune_ub) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_PRUNED;   // early prune (R16)
-        else if (it == k.max_iters) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_MAXITER;
+        else if (s.it0[nd] + it >= k.max_iters) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_MAXITER;
         s.flags[nd] = fl;
         if (blockIdx.x == 0) {
           k.nodef[nd * 4 + 0] = lbb;
           k.nodef[nd * 4 + 1] = primal;
           k.nodef[nd * 4 + 3] = dual;
           k.nodei[nd * 2 + 0] = fl;
-          k.nodei[nd * 2 + 1] = it;
+          k.nodei[nd * 2 + 1] = s.it0[nd] + it;
         }
       }
     }
@@ -1027,6 +1039,19 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     unsigned am = 0;
     for (int nd = 0; nd < kBC; nd++) am |= (s.flags[nd] & F_ACTIVE) ? 1u << nd : 0u;
     if (!am) break;
+    // continuous batching (§8(f) rank 2): few nodes left in this launch — suspend them here (their
+    // β, v, best dual and iteration count go back to the caller, which resumes them bitwise where
+    // they stopped, next to fresh nodes); only at regular checks, so resumed nodes stay on the
+    // check_every grid
+    if (k.suspend_at > 0 && it % k.check_every == 0 && it >= k.susp_min && __popc(am) <= k.suspend_at) {
+      if (tid < kBC && (s.flags[tid] & F_ACTIVE)) {
+        const int fl = (s.flags[tid] & ~F_ACTIVE) | F_SUSP;
+        s.flags[tid] = fl;
+        if (blockIdx.x == 0) k.nodei[tid * 2 + 0] = fl;
+      }
+      __syncthreads();
+      break;
+    }
     // ≤ 8 active nodes spread over both halves: move them into half 0 (the next sweep then runs
     // in single-half mode on every SM instead of paired); at most once per launch
     if (k.compact && nswp == 0 && __popc(am) <= 8 && (am & 0xFFu) && (am & 0xFF00u)) {
@@ -1057,7 +1082,9 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
     k.out_lb[nd] = fmax(lbb, plb);
     k.out_primal[nd] = k.nodef[nd * 4 + 1];
     k.out_iters[nd] = k.nodei[nd * 2 + 1];
-    k.out_flags[nd] = (uint8_t)(s.flags[nd] & (L0L2_FLAG_CONVERGED | L0L2_FLAG_MAXITER | L0L2_FLAG_PRUNED));
+    k.out_flags[nd] = (uint8_t)((s.flags[nd] & (L0L2_FLAG_CONVERGED | L0L2_FLAG_MAXITER | L0L2_FLAG_PRUNED)) |
+                                ((s.flags[nd] & F_SUSP) ? kFlagSuspended : 0));
+    if (k.out_lbbest) k.out_lbbest[nd] = lbb;
   }
 }
 
@@ -1098,15 +1125,16 @@ __global__ void scatter_fix(int nb, const int64_t* __restrict__ off, const int32
   }
 }
 
-__global__ void init_nodes(int nb, unsigned mask, unsigned cold, const double* parent_lb, double* nodef, int* nodei) {
+__global__ void init_nodes(int nb, unsigned mask, unsigned cold, const double* parent_lb, const double* lbbest_in,
+                           const int* it0_in, double* nodef, int* nodei) {
   const int nd = threadIdx.x;
   if (nd >= kBC) return;
-  nodef[nd * 4 + 0] = -INFINITY;
+  nodef[nd * 4 + 0] = (nd < nb && lbbest_in) ? lbbest_in[nd] : -INFINITY;
   nodef[nd * 4 + 1] = INFINITY;
   nodef[nd * 4 + 2] = (nd < nb && parent_lb) ? parent_lb[nd] : -INFINITY;
   nodef[nd * 4 + 3] = -INFINITY;
   nodei[nd * 2 + 0] = (nd < nb && ((mask >> nd) & 1u)) ? (F_ACTIVE | (((cold >> nd) & 1u) ? F_COLD : 0)) : 0;
-  nodei[nd * 2 + 1] = 0;
+  nodei[nd * 2 + 1] = (nd < nb && it0_in) ? it0_in[nd] : 0;
 }
 
 // ẑ, integrality, branch index (R10), support F1 ∪ {ẑ ≥ ½}
@@ -1238,7 +1266,7 @@ int debug_prof(unsigned long long*, int) { return 0; }
 
 size_t admm_smem_bytes(int64_t ld) {
   return sizeof(double) * ((size_t)NST * kPt * ld + NST * STQ + 2 * NMW * 64 + 2 * 8 * 12 + 2 * 64 * 4 + kBC) +
-         (NST + 4) * sizeof(uint64_t) + 2 * kBC * sizeof(int) + (2 * NST + 12) * sizeof(int) + NST * sizeof(unsigned) + 64;
+         (NST + 4) * sizeof(uint64_t) + 3 * kBC * sizeof(int) + (2 * NST + 12) * sizeof(int) + NST * sizeof(unsigned) + 64;
 }
 
 int admm_alloc(Ctx* c) {
@@ -1359,11 +1387,14 @@ int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st) {
 }
 
 int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
-  init_nodes<<<1, 32, 0, st>>>(a.nb, mask, a.cold_mask, a.parent_lb, c->node_f, c->node_i);
+  init_nodes<<<1, 32, 0, st>>>(a.nb, mask, a.cold_mask, a.parent_lb, a.lbbest_in, a.it0_in, c->node_f, c->node_i);
   L0L2_LAUNCHED(c);
   KP k{};
   k.act_mask = mask;
   k.prune_ub = a.prune_ub;
+  k.suspend_at = a.suspend_at;
+  k.susp_min = a.susp_min;
+  k.out_lbbest = a.out_lbbest;
   k.compact = 1;
   if (const char* e = getenv("L0L2_COMPACT")) k.compact = atoi(e) != 0;   // tuning / test hook
   k.Z = c->direct ? c->D : c->Z;

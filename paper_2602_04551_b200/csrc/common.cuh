@@ -151,8 +151,16 @@ struct BoundArgs {
   int *iters;                   // device [nb]
   uint8_t* flags;               // device [nb]
   double prune_ub = INFINITY;   // stop a node once its best dual reaches this (early prune, R16)
-  unsigned cold_mask = 0;       // nodes without a parent state: start at β = v = 0, no refresh (R6)
+  unsigned cold_mask = 0;       // nodes without a parent state: start at β = v = 0, no refresh (R6);
+                                // also resumed nodes (their state continues as is)
+  // continuous batching (§8(f) rank 2, solve.cu): resumed nodes' best dual and iterations so far
+  // (device [nb] or null), where the launch writes them back, and the suspension rule
+  const double* lbbest_in = nullptr;
+  const int* it0_in = nullptr;
+  double* out_lbbest = nullptr;
+  int suspend_at = 0, susp_min = 0;
 };
+constexpr uint8_t kFlagSuspended = 16;   // node flag: suspended by continuous batching (internal)
 int pack_group(Ctx* c, int nb, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
                const double* const* warm_ptrs_dev, cudaStream_t st);
 int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st);

@@ -96,7 +96,14 @@ struct Node {
   std::vector<int32_t> fidx;
   std::vector<uint8_t> fval;
   int slot;   // warm state slot (−1 = cold)
+  // continuous batching: a suspended node resumes from its own state with these
+  double lbbest = -INFINITY;   // running max of its checked duals (R7)
+  int32_t it0 = 0;             // ADMM iterations already run
+  int64_t parent = -1;         // trace: parent id and the fixing that created the node (2j + value)
+  int64_t lastfix = -1;
 };
+constexpr int kTraceRec = 10;   // doubles per l0l2_solve_trace record
+
 struct NodeCmp {   // min-heap by (lb, id)
   bool operator()(const Node& a, const Node& b) const { return a.lb != b.lb ? a.lb > b.lb : a.id > b.id; }
 };
@@ -151,6 +158,8 @@ struct RoundBufs {
   int32_t* fix_idx = nullptr;
   uint8_t* fix_val = nullptr;
   double* parent_lb = nullptr;
+  double *lbbest_in = nullptr, *lbbest_out = nullptr;
+  int32_t* it0_in = nullptr;
   double *lb = nullptr, *primal = nullptr, *obj = nullptr, *beta_s = nullptr;
   int32_t *iters = nullptr, *branch = nullptr, *scnt = nullptr, *sidx = nullptr, *cidx = nullptr;
   int64_t* soff = nullptr;
@@ -199,6 +208,7 @@ struct Solver {
   SlotPool pool;
   RoundBufs d;
   std::priority_queue<Node, std::vector<Node>, NodeCmp> open;
+  std::vector<Node> running;       // continuous batching: suspended nodes (resumed first)
   double UB = 0.0;                 // pruning threshold (≤ inc_ub: may be a global UB adopted from a peer)
   double inc_ub = 0.0;             // objective of the incumbent vector (inc_S, inc_b) held by this rank
   std::vector<int32_t> inc_S;
@@ -213,6 +223,8 @@ struct Solver {
   int64_t id_counter = 0, id_base = 0;
   int ub_owner = 0;
   int64_t moved = 0;   // nodes this rank sent away by rebalancing
+  int64_t suspensions = 0;   // continuous batching: node suspensions (each resumed later)
+  int64_t launch_slots = 0, launch_sweeps = 0;   // lane utilisation: Σ node-iterations / (16 · sweeps)
 
   int64_t new_id() {
     if (!partitioned) return next_id++;
@@ -224,8 +236,8 @@ struct Solver {
     const int64_t p = c->p;
     size_t need = 0;
     auto sz = [&](size_t b) { need += (b + 255) / 256 * 256; };
-    sz(sizeof(int64_t) * (Bmax + 1)); for (int i = 0; i < 4; i++) sz(sizeof(double) * Bmax);
-    for (int i = 0; i < 3; i++) sz(sizeof(int32_t) * Bmax);
+    sz(sizeof(int64_t) * (Bmax + 1)); for (int i = 0; i < 6; i++) sz(sizeof(double) * Bmax);
+    for (int i = 0; i < 4; i++) sz(sizeof(int32_t) * Bmax);
     sz(sizeof(int32_t) * (size_t)kBC * p); sz(sizeof(int64_t) * (Bmax + 1)); sz(Bmax); sz(sizeof(double*) * 2 * kBC);
     if (c->solve_buf_B < Bmax) {
       if (c->solve_buf) cudaFree(c->solve_buf);
@@ -242,6 +254,9 @@ struct Solver {
     auto A = [&](size_t b) { void* r = cur; cur += (b + 255) / 256 * 256; return r; };
     d.fix_off = (int64_t*)A(sizeof(int64_t) * (Bmax + 1));
     d.parent_lb = (double*)A(sizeof(double) * Bmax);
+    d.lbbest_in = (double*)A(sizeof(double) * Bmax);
+    d.lbbest_out = (double*)A(sizeof(double) * Bmax);
+    d.it0_in = (int32_t*)A(sizeof(int32_t) * Bmax);
     d.lb = (double*)A(sizeof(double) * Bmax);
     d.primal = (double*)A(sizeof(double) * Bmax);
     d.obj = (double*)A(sizeof(double) * Bmax);
@@ -263,6 +278,8 @@ struct Solver {
     double lb, primal, obj;
     int32_t iters, branch;
     uint8_t flags;
+    bool susp;        // suspended by continuous batching: resumes later from slot
+    double lbbest;
     std::vector<int32_t> supp;
     std::vector<double> beta_s;
     int slot;
@@ -278,12 +295,17 @@ struct Solver {
     std::vector<int64_t> off(B + 1, 0);
     std::vector<int32_t> fidx;
     std::vector<uint8_t> fval;
-    std::vector<double> plb(B);
+    std::vector<double> plb(B), lbb(B);
+    std::vector<int32_t> it0(B);
+    bool resumed = false;
     for (int k = 0; k < B; k++) {
       fidx.insert(fidx.end(), batch[k].fidx.begin(), batch[k].fidx.end());
       fval.insert(fval.end(), batch[k].fval.begin(), batch[k].fval.end());
       off[k + 1] = (int64_t)fidx.size();
       plb[k] = batch[k].lb;
+      lbb[k] = batch[k].lbbest;
+      it0[k] = batch[k].it0;
+      resumed |= batch[k].it0 > 0;
     }
     int32_t* dfi = (int32_t*)c->scratch_n(2, sizeof(int32_t) * std::max<size_t>(1, fidx.size()));
     uint8_t* dfv = (uint8_t*)c->scratch_n(3, std::max<size_t>(1, fval.size()));
@@ -294,6 +316,10 @@ struct Solver {
       L0L2_CUDA(c, cudaMemcpyAsync(dfv, fval.data(), fval.size(), cudaMemcpyHostToDevice, st));
     }
     L0L2_CUDA(c, cudaMemcpyAsync(d.parent_lb, plb.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+    if (resumed) {
+      L0L2_CUDA(c, cudaMemcpyAsync(d.lbbest_in, lbb.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+      L0L2_CUDA(c, cudaMemcpyAsync(d.it0_in, it0.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice, st));
+    }
     std::vector<int32_t> scnt(B);
     for (int g0 = 0; g0 < B; g0 += kBC) {
       const int nb = std::min(kBC, B - g0);
@@ -309,8 +335,16 @@ struct Solver {
       int rc = pack_group(c, nb, d.fix_off + g0, dfi, dfv, (const double* const*)d.wptr, st);
       if (rc) return rc;
       BoundArgs a{nb, d.parent_lb + g0, d.lb + g0, d.primal + g0, d.iters + g0, d.flags + g0};
-      for (int k = 0; k < nb; k++) if (!hp[k]) a.cold_mask |= 1u << k;
+      // cold: no parent state, or a resumed node (its own state continues, no refresh)
+      for (int k = 0; k < nb; k++) if (!hp[k] || batch[g0 + k].it0 > 0) a.cold_mask |= 1u << k;
       if (o.early_prune) a.prune_ub = UB * (1.0 - 1e-12);   // UB of the round's start (R16)
+      if (resumed) { a.lbbest_in = d.lbbest_in + g0; a.it0_in = d.it0_in + g0; }
+      a.out_lbbest = d.lbbest_out + g0;
+      // continuous batching: suspend the last few nodes of a launch while others are waiting
+      if (o.continuous > 0 && W == 1 && !open.empty()) {
+        a.suspend_at = o.continuous;
+        a.susp_min = 2 * c->check_every;
+      }
       if ((rc = run_admm(c, a, st))) return rc;
       if ((rc = finalize_group(c, nb, nullptr, d.branch + g0, d.flags + g0, d.scnt + g0, d.sidx, p, st))) return rc;
       if ((rc = unpack_warm(c, nb, d.wptr + kBC, st))) return rc;
@@ -327,10 +361,11 @@ struct Solver {
                                        cudaMemcpyDeviceToHost, st));
       }
     }
-    std::vector<double> hlb(B), hpr(B);
+    std::vector<double> hlb(B), hpr(B), hlbb(B);
     std::vector<int32_t> hit(B), hbr(B);
     std::vector<uint8_t> hfl(B);
     L0L2_CUDA(c, cudaMemcpyAsync(hlb.data(), d.lb, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(hlbb.data(), d.lbbest_out, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
     L0L2_CUDA(c, cudaMemcpyAsync(hpr.data(), d.primal, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
     L0L2_CUDA(c, cudaMemcpyAsync(hit.data(), d.iters, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
     L0L2_CUDA(c, cudaMemcpyAsync(hbr.data(), d.branch, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
@@ -339,11 +374,12 @@ struct Solver {
     // the parents' warm states have been consumed by pack_group
     for (int k = 0; k < B; k++) pool.release(batch[k].slot);
     t_bound += secs(t0);
-    // ---- upper bounds on the rounded supports
+    // ---- upper bounds on the rounded supports of the nodes that finished
     auto t1 = Clock::now();
     std::vector<int64_t> so(B + 1, 0);
     std::vector<int32_t> sall;
     for (int k = 0; k < B; k++) {
+      if (hfl[k] & kFlagSuspended) res[k].supp.clear();
       sall.insert(sall.end(), res[k].supp.begin(), res[k].supp.end());
       so[k + 1] = (int64_t)sall.size();
     }
@@ -369,9 +405,12 @@ struct Solver {
       r.flags = hfl[k];
       r.obj = hob[k];
       r.beta_s.assign(hbs.begin() + so[k], hbs.begin() + so[k + 1]);
+      r.susp = (r.flags & kFlagSuspended) != 0;
+      r.lbbest = hlbb[k];
+      if (r.susp) r.obj = INFINITY;
       if (r.flags & L0L2_FLAG_MAXITER) notconv = true;
-      nodes++;
-      node_iters += r.iters;
+      if (!r.susp) nodes++;
+      node_iters += r.iters - batch[k].it0;
     }
     t_upper += secs(t1);
     return L0L2_OK;
@@ -384,7 +423,7 @@ struct Solver {
     for (int k = 0; k < B; k++) order[k] = k;
     std::sort(order.begin(), order.end(), [&](int a, int b) { return batch[a].id < batch[b].id; });
     for (int k : order)
-      if (res[k].obj < UB) {
+      if (!res[k].susp && res[k].obj < UB) {
         UB = inc_ub = res[k].obj;
         inc_S = res[k].supp;
         inc_b = res[k].beta_s;
@@ -392,12 +431,24 @@ struct Solver {
     if (trace)
       for (int k : order) {
         const Res& r = res[k];
-        const double rec[8] = {(double)batch[k].id, (double)batch[k].depth, r.lb, r.primal, (double)r.iters,
-                               (double)r.branch, (double)r.flags, r.obj};
-        trace->insert(trace->end(), rec, rec + 8);
+        if (r.susp) continue;
+        const double rec[kTraceRec] = {(double)batch[k].id, (double)batch[k].depth, r.lb, r.primal, (double)r.iters,
+                                       (double)r.branch, (double)r.flags, r.obj, (double)batch[k].parent,
+                                       (double)batch[k].lastfix};
+        trace->insert(trace->end(), rec, rec + kTraceRec);
       }
     for (int k : order) {
       Res& r = res[k];
+      if (r.susp) {   // continuous batching: resumes in a later launch from its own state
+        Node u = batch[k];
+        u.lb = r.lb;
+        u.lbbest = r.lbbest;
+        u.it0 = r.iters;
+        u.slot = r.slot;
+        running.push_back(std::move(u));
+        suspensions++;
+        continue;
+      }
       const bool integral = (r.flags & L0L2_FLAG_INTEGRAL) != 0;
       const bool pruned = r.lb >= UB * (1.0 - 1e-12) || integral || r.branch < 0;
       if (pruned) {
@@ -413,6 +464,9 @@ struct Solver {
       b.fval.push_back(1);   // F1 ∪ {j}
       a.id = new_id();
       b.id = new_id();
+      a.parent = b.parent = u.id;
+      a.lastfix = 2 * (int64_t)r.branch;
+      b.lastfix = 2 * (int64_t)r.branch + 1;
       pool.addref(r.slot);   // two children share the parent's state (ref 1 → 2)
       open.push(std::move(a));
       open.push(std::move(b));
@@ -421,6 +475,14 @@ struct Solver {
   }
 
   void prune_open() {
+    {   // suspended nodes whose bound already prunes them
+      std::vector<Node> keep;
+      for (auto& u : running) {
+        if (u.lb >= UB * (1.0 - 1e-12)) pool.release(u.slot);
+        else keep.push_back(std::move(u));
+      }
+      running.swap(keep);
+    }
     std::vector<Node> keep;
     keep.reserve(open.size());
     while (!open.empty()) {
@@ -432,7 +494,12 @@ struct Solver {
     for (auto& u : keep) open.push(std::move(u));
   }
 
-  double local_lbmin() const { return open.empty() ? INFINITY : open.top().lb; }
+  double local_lbmin() const {
+    double m = open.empty() ? INFINITY : open.top().lb;
+    for (const auto& u : running) m = std::min(m, u.lb);
+    return m;
+  }
+  int64_t local_open() const { return (int64_t)(open.size() + running.size()); }
 
   // ---- multi-rank helpers.  The carrier is NCCL (device buffers on the solve stream) or the
   // caller's host transport (l0l2_comm_init_transport); the exchange logic is the same.
@@ -659,6 +726,7 @@ void l0l2_default_solve_opts(l0l2_solve_opts* o) {
   o->record = 0;
   o->init_mp = 0;
   o->early_prune = 0;
+  o->continuous = 0;
 }
 
 int l0l2_nccl_unique_id(uint8_t out[128]) {
@@ -710,8 +778,8 @@ int l0l2_comm_init_transport(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const 
 int64_t l0l2_solve_trace(const l0l2_ctx* ctx, double* rec, int64_t max_nodes) {
   if (!ctx) return -1;
   const std::vector<double>& t = ctx->impl.trace;
-  const int64_t n = (int64_t)t.size() / 8;
-  if (rec && max_nodes > 0) std::memcpy(rec, t.data(), sizeof(double) * 8 * std::min(n, max_nodes));
+  const int64_t n = (int64_t)t.size() / kTraceRec;
+  if (rec && max_nodes > 0) std::memcpy(rec, t.data(), sizeof(double) * kTraceRec * std::min(n, max_nodes));
   return n;
 }
 
@@ -803,7 +871,7 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
     S.prune_open();
     S.t_tree += secs(tt);
     double gUB = S.UB, gLB;
-    int64_t gopen = (int64_t)S.open.size(), gnodes = S.nodes;
+    int64_t gopen = S.local_open(), gnodes = S.nodes;
     double elapsed = secs(T0);
     if (S.W > 1) {
       Status mine{S.UB, S.local_lbmin(), (double)S.open.size(), (double)S.nodes, (double)S.node_iters, elapsed,
@@ -853,6 +921,8 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
       }
     }
     std::vector<Node> batch;
+    for (auto& u : S.running) batch.push_back(std::move(u));   // suspended nodes resume first
+    S.running.clear();
     while (!S.open.empty() && (int)batch.size() < o.batch) {
       batch.push_back(S.open.top());
       S.open.pop();
@@ -896,6 +966,7 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
     stats->nodes_global = S.nodes;
     stats->node_iters_global = S.node_iters;
     stats->nodes_moved = S.moved;
+    stats->suspensions = S.suspensions;
     if (S.W > 1) {
       stats->nodes_moved = 0;
       for (int r = 0; r < S.W; r++) stats->nodes_moved += (int64_t)all[r].pad;
