@@ -75,6 +75,7 @@ struct KP {
   int ntiles, nsr, nb, check_every, max_iters, pfd;   // nsr: tile sub-ranges (= grid)
   unsigned act_mask;               // node slots run by this launch (outputs written for these only)
   double prune_ub;                 // early prune threshold (R16; +inf = off)
+  const double* prune_ub_dev;      // or read from device memory at launch (device frontier), if set
   int suspend_at;                  // continuous batching: at a check with ≤ suspend_at active nodes (and
                                    // ≥ susp_min iterations in this launch) the launch suspends them (0 = off)
   int susp_min;
@@ -475,18 +476,29 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
       PROF_ACC(0);
       if (tile < 0) return false;
       const double* T = s.tiles + (size_t)(m % NST) * kPt * ld + cA * ld + kA;
-      double sc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#ifndef L0L2_ADJ_CHAINS
+#define L0L2_ADJ_CHAINS 4
+#endif
+      constexpr int NCH = L0L2_ADJ_CHAINS;   // independent DMMA accumulator chains of the adjoint
+      double sc[NCH][2];
+#pragma unroll
+      for (int c = 0; c < NCH; c++) sc[c][0] = sc[c][1] = 0.0;
 #pragma unroll
 // EXP_NOADJ / EXP_NOFWD / EXP_NOEPI: timing experiments only (the results are wrong), built with
 // tools/build_variant.py — they compile out the adjoint DMMAs, the forward DMMAs or the epilogue math
 // to measure what the tile pipeline costs without them.
 #ifndef EXP_NOADJ
-      for (int i = 0; i < KS; i++) dmma(sc[i & 3], T[4 * (warp + NMW * i)], uf[i]);
+      for (int i = 0; i < KS; i++) dmma(sc[i % NCH], T[4 * (warp + NMW * i)], uf[i]);
 #endif
       double* sp = s.spart + (m & 1) * NMW * 64 + warp * 64;
       // C fragment: row (col j) = lane>>2, cols (node) = 2*(lane&3) + {0,1}
-      sp[cA * 8 + 2 * kA] = (sc[0][0] + sc[1][0]) + (sc[2][0] + sc[3][0]);
-      sp[cA * 8 + 2 * kA + 1] = (sc[0][1] + sc[1][1]) + (sc[2][1] + sc[3][1]);
+      if (NCH == 4) {
+        sp[cA * 8 + 2 * kA] = (sc[0][0] + sc[1][0]) + (sc[2 % NCH][0] + sc[3 % NCH][0]);
+        sp[cA * 8 + 2 * kA + 1] = (sc[0][1] + sc[1][1]) + (sc[2 % NCH][1] + sc[3 % NCH][1]);
+      } else {
+        sp[cA * 8 + 2 * kA] = sc[0][0] + sc[1 % NCH][0];
+        sp[cA * 8 + 2 * kA + 1] = sc[0][1] + sc[1 % NCH][1];
+      }
       mbar_arrive_warp(&s.sready[m & 1]);
       PROF_ACC(1);
       return true;
@@ -888,7 +900,8 @@ __device__ void swap_slots(const KP& k, Smem& s, const int* pa, const int* pb, i
 
 // DIR: the direct regime (R17) as a separate instantiation, so the Z-form code is unchanged by it
 template <int KS, int MT, bool DIR>
-__global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
+__global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k_in) {
+  KP k = k_in;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem s;
   {
@@ -929,6 +942,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k) {
 #ifdef L0L2_PROF
   if (tid < NW * 8) prof_s[tid / 8][tid % 8] = 0;
 #endif
+  if (k.prune_ub_dev) k.prune_ub = __ldcg(k.prune_ub_dev);   // (KP is the kernel's by-value copy)
   unsigned phases = 0, hph = 0;
   __shared__ int swp_a[8], swp_b[8];   // slot pairs exchanged by the compaction (same in every thread)
   int nswp = 0;
@@ -1125,10 +1139,26 @@ __global__ void scatter_fix(int nb, const int64_t* __restrict__ off, const int32
   }
 }
 
+// device frontier (frontier.cu): the fixings of node nd of a group as a chain of records
+// rec → {parent record, 2j + value}; codes F0 → 1, F1 → 2, and the warm edit β_j ← 0 on F0
+__global__ void scatter_chain(int nb, const int* __restrict__ node_rec, const int* __restrict__ recs, int rec_stride,
+                              double* stt) {
+  const int nd = blockIdx.x;
+  if (nd >= nb || threadIdx.x != 0) return;
+  for (int r = node_rec[nd]; r >= 0; r = recs[(int64_t)r * rec_stride]) {
+    const int fx = recs[(int64_t)r * rec_stride + 1];
+    const int64_t j = fx >> 1;
+    st_code(stt, j, nd) = (fx & 1) ? 2 : 1;
+    if (!(fx & 1)) stt[st_beta(j, nd)] = 0.0;
+  }
+}
+
 __global__ void init_nodes(int nb, unsigned mask, unsigned cold, const double* parent_lb, const double* lbbest_in,
-                           const int* it0_in, double* nodef, int* nodei) {
+                           const int* it0_in, const double* const* warm_ptrs, double* nodef, int* nodei) {
   const int nd = threadIdx.x;
   if (nd >= kBC) return;
+  // device frontier: a node without a parent state (null warm pointer) is cold
+  if (warm_ptrs && nd < nb && warm_ptrs[nd] == nullptr) cold |= 1u << nd;
   nodef[nd * 4 + 0] = (nd < nb && lbbest_in) ? lbbest_in[nd] : -INFINITY;
   nodef[nd * 4 + 1] = INFINITY;
   nodef[nd * 4 + 2] = (nd < nb && parent_lb) ? parent_lb[nd] : -INFINITY;
@@ -1387,11 +1417,13 @@ int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st) {
 }
 
 int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
-  init_nodes<<<1, 32, 0, st>>>(a.nb, mask, a.cold_mask, a.parent_lb, a.lbbest_in, a.it0_in, c->node_f, c->node_i);
+  init_nodes<<<1, 32, 0, st>>>(a.nb, mask, a.cold_mask, a.parent_lb, a.lbbest_in, a.it0_in, a.warm_ptrs, c->node_f,
+                               c->node_i);
   L0L2_LAUNCHED(c);
   KP k{};
   k.act_mask = mask;
   k.prune_ub = a.prune_ub;
+  k.prune_ub_dev = a.prune_ub_dev;
   k.suspend_at = a.suspend_at;
   k.susp_min = a.susp_min;
   k.out_lbbest = a.out_lbbest;
@@ -1446,6 +1478,11 @@ int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
 int account_admm(Ctx* c, int nb, const int* iters_host) {
   float ms = 0.f;
   L0L2_CUDA(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  account_admm_stats(c, nb, iters_host, ms);
+  return L0L2_OK;
+}
+
+void account_admm_stats(Ctx* c, int nb, const int* iters_host, float ms) {
   // iterations streamed = Σ over the launches (one, or one per node half when split) of
   // (max iterations of its nodes + the refresh sweep)
   const bool split = nb > 8 && !admm_paired(c);
@@ -1468,6 +1505,11 @@ int account_admm(Ctx* c, int nb, const int* iters_host) {
   c->ks.admm_ms += ms;
   c->ks.admm_bytes_alg += T * 8.0 * kn * p + 33.0 * p * (double)(tsum + nb);
   c->ks.admm_flops_alg += (double)(tsum + nb) * fl;
+}
+
+int scatter_chain_group(Ctx* c, int nb, const int* node_rec, const int* recs, int rec_stride, cudaStream_t st) {
+  scatter_chain<<<nb, 32, 0, st>>>(nb, node_rec, recs, rec_stride, c->stt);
+  L0L2_LAUNCHED(c);
   return L0L2_OK;
 }
 

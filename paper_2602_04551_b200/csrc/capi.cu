@@ -80,6 +80,7 @@ void l0l2_destroy(l0l2_ctx* ctx) {
   if (c->solve_stream) cudaStreamDestroy(c->solve_stream);
   for (auto e : c->ev) if (e) cudaEventDestroy(e);
   comm_free(c);
+  frontier_free(c);
   delete ctx;
 }
 

@@ -111,6 +111,7 @@ struct Ctx {
   int solve_buf_B = 0;
   cudaStream_t solve_stream = nullptr;
   size_t pool_cap = 0;
+  void* fr_state = nullptr;   // device frontier arrays (frontier.cu), kept across solves
 };
 
 int set_err(Ctx* c, int code, const char* fmt, ...);
@@ -159,15 +160,26 @@ struct BoundArgs {
   const int* it0_in = nullptr;
   double* out_lbbest = nullptr;
   int suspend_at = 0, susp_min = 0;
+  // device frontier (frontier.cu): cold bits from the device warm-pointer array (null = cold) and the
+  // early-prune threshold read from device memory at launch
+  const double* const* warm_ptrs = nullptr;
+  const double* prune_ub_dev = nullptr;
 };
 constexpr uint8_t kFlagSuspended = 16;   // node flag: suspended by continuous batching (internal)
 int pack_group(Ctx* c, int nb, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
                const double* const* warm_ptrs_dev, cudaStream_t st);
 int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st);
 int account_admm(Ctx* c, int nb, const int* iters_host);
+void account_admm_stats(Ctx* c, int nb, const int* iters_host, float ms);   // same, given the launch's time
+// device-frontier solve (frontier.cu): single rank, synchronous rounds
+void frontier_free(Ctx* c);
+int solve_device(Ctx* c, const l0l2_solve_opts& o, double* beta, double* obj, double* gap, l0l2_stats* stats);
 int finalize_group(Ctx* c, int nb, double* zhat, int32_t* branch_j, uint8_t* flags,
                    int32_t* supp_cnt, int32_t* supp_idx, int64_t supp_stride, cudaStream_t st);
 int unpack_warm(Ctx* c, int nb, double* const* warm_ptrs_dev, cudaStream_t st);
+// device frontier: apply the fixing chains (records {parent, 2j + value}, rec_stride ints apart) of a
+// packed group's nodes to its code plane / state (after pack_group with null fixings)
+int scatter_chain_group(Ctx* c, int nb, const int* node_rec, const int* recs, int rec_stride, cudaStream_t st);
 int dual_residual(Ctx* c, int nb, double* dual_r, int64_t ldr, cudaStream_t st);
 int upper_batch(Ctx* c, int B, const int64_t* supp_off, const int32_t* supp_idx, double* obj,
                 double* beta_s, cudaStream_t st);

@@ -801,6 +801,11 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
   else l0l2_default_solve_opts(&o);
   if (o.batch < 1) return set_err(c, L0L2_EINVAL, "batch < 1");
   L0L2_CUDA(c, cudaSetDevice(c->device));
+  // single rank, synchronous rounds: the frontier lives on the device (frontier.cu);
+  // L0L2_HOST_FRONTIER=1 selects this file's host frontier (test hook: the two give the same tree)
+  const char* hf = getenv("L0L2_HOST_FRONTIER");
+  if (c->nranks == 1 && o.continuous == 0 && o.batch <= 128 && !(hf && atoi(hf) != 0))
+    return solve_device(c, o, beta, obj, gap, stats);
   const auto T0 = Clock::now();
   Solver S{};
   S.c = c;
