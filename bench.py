@@ -85,9 +85,14 @@ def measured_peaks():
 def ncu_traffic():
     """dram bytes per ADMM launch from the committed ncu --set full capture summary, if any."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_admm_traffic.json")) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch_per_alg_byte")
+        # the ratio measured on a tree-step launch of this very step (tools/ncu_tree_step.py +
+        # tools/ncu_summary.py), else the round-1 fixed-iteration capture
+        for name in ("ncu_admm_tree_launch_r02.json", "ncu_admm_traffic.json"):
+            pth = os.path.join(ROOT, "profiles", name)
+            if os.path.exists(pth):
+                with open(pth) as f:
+                    return json.load(f).get("dram_bytes_per_launch_per_alg_byte")
+        return None
     except Exception:
         return None
 
@@ -337,11 +342,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # ranks sharing a GPU (e.g. a dry run of the multi-rank path on a 1-GPU box): NCCL refuses two ranks
+    # on one device, so the exchange goes through the library's host transport over gloo
+    shared = world > 1 and torch.cuda.device_count() < world
+    if shared:
+        local = local % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", local)
@@ -354,20 +367,23 @@ def main():
     def make_problem(Xh, yh):
         pr = Problem(Xh, yh, inst.lambda0, inst.lambda2, inst.M, rho=rho, node_tol=args.node_tol,
                      max_iters=10000, device=local)
-        pr.init_distributed()
+        pr.init_distributed(transport="host" if shared else "nccl")
         return pr
 
     def barrier():
         torch.cuda.synchronize(dev)
         if world > 1:
             import torch.distributed as dist
-            dist.barrier(device_ids=[local])
+            if shared:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
 
     def max_over_ranks(x):
         if world == 1:
             return x
         import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -375,7 +391,7 @@ def main():
         if world == 1:
             return x
         import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -593,7 +609,10 @@ def main():
                 "config": {"workload": "%s seed %d: %s" % (args.config, args.seed, CONFIG_DESC[args.config]),
                            "lambda0": inst.lambda0, "lambda2": inst.lambda2, "M": inst.M, "rho": rho,
                            "gap_tol": args.gap_tol, "node_tol": args.node_tol, "node_limit": args.node_limit,
-                           "batch": args.batch, "parallelism": "frontier partitioned over %d GPU(s)" % world,
+                           "batch": args.batch,
+                           "parallelism": ("frontier partitioned over %d GPU(s)" % world) if not shared else
+                           ("DRY RUN: %d ranks share %d GPU(s), exchange over the host transport (gloo)"
+                            % (world, torch.cuda.device_count())),
                            "l2": "inputs larger than L2 (X and Z are %.0f MB each)" % (inst.X.nbytes / 2 ** 20)},
                 "time_per_step_s": ms / args.steps / 1e3,
                 # null unless the timed step itself certifies its gap (the C4 prefix does not);
