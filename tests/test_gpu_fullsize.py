@@ -172,3 +172,37 @@ def test_consecutive_checks(ce, mi):
         r = O.admm_node(P, O.make_code(inst.p, *fx[k]), node_tol=1e-7, max_iters=mi, check_every=ce)
         assert int(out["iters"][k]) == r.iters
         assert abs(float(out["lb"][k]) - r.lb) <= 1e-6 * max(1.0, abs(r.lb))
+
+
+def test_c4_certified_solve_oracle_evidence():
+    """North-star target (NS-T9): the certified C4 solve of bench.py's certified_c4 (n=1000, p=1e5,
+    λ0 = 2λ0*, gap 1e-2, node_tol 1e-4, B = 16, ρ = 3·mean‖X_j‖²).  Oracle evidence:
+    * its first 111 nodes (10 rounds) equal the oracle's own BnB on the same instance node for node
+      (tests/golden/oracle_C4_l0x2_tree_g0.01_n0.0001_B16_lim96.json, written by
+      tools/oracle_tree_golden.py from oracle/ only, 36 CPU-minutes): ids, LBs 1e-6, iterations,
+      branches, UBs 1e-6;
+    * the returned objective is the oracle's exact box ridge on the returned support (1e-9), the
+      support is the planted β† support, and the certified LB ≤ that objective with gap ≤ 1e-2."""
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_C4_l0x2_tree_g0.01_n0.0001_B16_lim96.json")))
+    inst = synth.config_instance("C4", seed=0, lambda0_mult=2.0)
+    assert abs(inst.lambda0 - g["lambda0"]) <= 1e-12 * g["lambda0"]
+    prob = Problem(np.asfortranarray(inst.X), inst.y, inst.lambda0, inst.lambda2, inst.M, rho=g["rho"],
+                   node_tol=g["node_tol"])
+    res = prob.l0l2_solve(gap_tol=g["gap_tol"], batch=g["batch"], record=True)
+    prob.close()
+    gt = {t["id"]: t for t in res["trace"]}
+    for t in g["trace"]:
+        u = gt.get(t["id"])
+        assert u is not None, ("node missing on GPU", t["id"])
+        assert abs(u["lb"] - t["lb"]) <= 1e-6 * max(1.0, abs(t["lb"])), (t["id"], u["lb"], t["lb"])
+        assert u["iters"] == t["iters"], (t["id"], u["iters"], t["iters"])
+        assert u["branch_j"] == t["branch_j"], (t["id"], u["branch_j"], t["branch_j"])
+        assert abs(u["ub"] - t["ub"]) <= 1e-6 * abs(t["ub"]), (t["id"], u["ub"], t["ub"])
+    st = res["stats"]
+    assert st["status"] <= 1 and res["gap"] <= g["gap_tol"]
+    assert np.array_equal(res["support"], inst.support_true)
+    P = O.Problem(inst.X, inst.y, inst.lambda0, inst.lambda2, inst.M, rho=g["rho"])
+    ref, bS = O.upper_bound(P, res["support"])
+    assert abs(res["obj"] - ref) <= 1e-9 * abs(ref), (res["obj"], ref)
+    assert rel(res["beta"][res["support"]], bS) < 1e-6
+    assert st["lb"] <= ref * (1 + 1e-12)
