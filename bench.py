@@ -457,14 +457,18 @@ def main():
               "note": "one HBM pass over X (8np bytes) per round + O(|S|n) backward work; host reads one flag per round"}
     prob.close()
     del prob
+    section_errors = {}
     micro = micro3 = None
-    if world == 1 and not args.no_microbench:
-        micro = bound_microbench(inst, rho, local, args.micro_iters)
-        if args.config == "C4":   # SURVEY §8(d) asks for C3 too: Z = 80 MB, L2-resident
-            inst3, _ = load_instance("C3", args.seed)
-            rho3 = float(np.mean(np.einsum("ij,ij->j", inst3.X, inst3.X))) * args.rho_mult
-            micro3 = bound_microbench(inst3, rho3, local, args.micro_iters)
-            micro3["workload"] = "C3 (n=1000, p=1e4; Z is L2-resident): " + micro3["workload"]
+    try:
+        if world == 1 and not args.no_microbench:
+            micro = bound_microbench(inst, rho, local, args.micro_iters)
+            if args.config == "C4":   # SURVEY §8(d) asks for C3 too: Z = 80 MB, L2-resident
+                inst3, _ = load_instance("C3", args.seed)
+                rho3 = float(np.mean(np.einsum("ij,ij->j", inst3.X, inst3.X))) * args.rho_mult
+                micro3 = bound_microbench(inst3, rho3, local, args.micro_iters)
+                micro3["workload"] = "C3 (n=1000, p=1e4; Z is L2-resident): " + micro3["workload"]
+    except Exception as e:   # context sections never cost the headline line
+        section_errors['micro'] = repr(e)
 
     # ------------------------------------------------------------------ end-to-end arm (host buffers)
     import torch as _t
@@ -498,109 +502,121 @@ def main():
     # time-to-certified-optimality half of the metric is measured on C2 (n = p = 1000), which the
     # solver certifies: gap_tol 1e-2 / node_tol 1e-4 (paper) and 1e-6 / 1e-8, X resident.
     certified = None
-    if world == 1 and not args.no_certified:
-        certified = []
-        for cfg2 in args.certified_configs.split(","):
-            inst2, _ = load_instance(cfg2, args.seed)
-            rho2 = float(np.mean(np.einsum("ij,ij->j", inst2.X, inst2.X))) * args.rho_mult
-            block = {"workload": "%s seed %d: %s" % (cfg2, args.seed, CONFIG_DESC[cfg2]), "runs": []}
-            # the paper's synchronous Algorithm 1, then with the §8(f) options (MP incumbent, early prune)
-            for gt_, nt_, ext in ((1e-2, 1e-4, False), (1e-6, 1e-8, False), (1e-2, 1e-4, True), (1e-6, 1e-8, True)):
-                pr2 = Problem(np.asfortranarray(inst2.X), inst2.y, inst2.lambda0, inst2.lambda2, inst2.M, rho=rho2,
-                              node_tol=nt_, max_iters=10000, device=local)
-                kw = dict(gap_tol=gt_, batch=args.batch, init_mp=ext, early_prune=ext, time_limit_s=60.0)
-                pr2.l0l2_solve(**kw)   # warm-up
-                torch.cuda.synchronize(dev)
-                t = time.perf_counter()
-                r2 = pr2.l0l2_solve(**kw)
-                dt2 = time.perf_counter() - t
-                st2 = r2["stats"]
-                block["runs"].append({"gap_tol": gt_, "node_tol": nt_, "init_mp": ext, "early_prune": ext,
-                                      "node_iters": st2["node_iters"], "time_to_certified_optimality_s": dt2,
-                                      "certified": st2["status"] <= 1, "gap": r2["gap"], "nodes": st2["nodes"],
-                                      "nodes_per_s": st2["nodes"] / dt2, "objective": r2["obj"],
-                                      "support": [int(j) for j in r2["support"]]})
-                pr2.close()
-            certified.append(block)
-        # seeds 0-9 of C2 (the paper averages 10 seeds): median and IQR of the certified solve
-        if "C2" in args.certified_configs.split(",") and args.seeds > 1:
-            seeds_blk = {"workload": "C2 seeds 0-%d: %s" % (args.seeds - 1, CONFIG_DESC["C2"]), "gap_tol": 1e-6,
-                         "node_tol": 1e-8, "batch": args.batch, "runs": []}
-            for ext in (False, True):
-                ts, ns = [], []
-                for sd in range(args.seeds):
-                    inst2, _ = load_instance("C2", sd)
-                    rho2 = float(np.mean(np.einsum("ij,ij->j", inst2.X, inst2.X))) * args.rho_mult
-                    pr2 = Problem(np.asfortranarray(inst2.X), inst2.y, inst2.lambda0, inst2.lambda2, inst2.M,
-                                  rho=rho2, node_tol=1e-8, max_iters=10000, device=local)
-                    kw = dict(gap_tol=1e-6, batch=args.batch, init_mp=ext, early_prune=ext, time_limit_s=60.0)
+    try:
+        if world == 1 and not args.no_certified:
+            certified = []
+            for cfg2 in args.certified_configs.split(","):
+                inst2, _ = load_instance(cfg2, args.seed)
+                rho2 = float(np.mean(np.einsum("ij,ij->j", inst2.X, inst2.X))) * args.rho_mult
+                block = {"workload": "%s seed %d: %s" % (cfg2, args.seed, CONFIG_DESC[cfg2]), "runs": []}
+                # the paper's synchronous Algorithm 1, then with the §8(f) options (MP incumbent, early prune)
+                for gt_, nt_, ext in ((1e-2, 1e-4, False), (1e-6, 1e-8, False), (1e-2, 1e-4, True), (1e-6, 1e-8, True)):
+                    pr2 = Problem(np.asfortranarray(inst2.X), inst2.y, inst2.lambda0, inst2.lambda2, inst2.M, rho=rho2,
+                                  node_tol=nt_, max_iters=10000, device=local)
+                    kw = dict(gap_tol=gt_, batch=args.batch, init_mp=ext, early_prune=ext, time_limit_s=60.0)
                     pr2.l0l2_solve(**kw)   # warm-up
                     torch.cuda.synchronize(dev)
                     t = time.perf_counter()
                     r2 = pr2.l0l2_solve(**kw)
                     dt2 = time.perf_counter() - t
+                    st2 = r2["stats"]
+                    block["runs"].append({"gap_tol": gt_, "node_tol": nt_, "init_mp": ext, "early_prune": ext,
+                                          "node_iters": st2["node_iters"], "time_to_certified_optimality_s": dt2,
+                                          "certified": st2["status"] <= 1, "gap": r2["gap"], "nodes": st2["nodes"],
+                                          "nodes_per_s": st2["nodes"] / dt2, "objective": r2["obj"],
+                                          "support": [int(j) for j in r2["support"]]})
                     pr2.close()
-                    if r2["stats"]["status"] <= 1:
-                        ts.append(dt2)
-                    ns.append(r2["stats"]["nodes"])
-                q = np.percentile(ts, [25, 50, 75]) if ts else [None] * 3
-                seeds_blk["runs"].append({"init_mp": ext, "early_prune": ext, "certified": len(ts),
-                                          "time_s_median": q[1], "time_s_iqr": [q[0], q[2]],
-                                          "nodes_median": float(np.median(ns)), "times_s": ts, "nodes": ns})
-            certified.append(seeds_blk)
+                certified.append(block)
+            # seeds 0-9 of C2 (the paper averages 10 seeds): median and IQR of the certified solve
+            if "C2" in args.certified_configs.split(",") and args.seeds > 1:
+                seeds_blk = {"workload": "C2 seeds 0-%d: %s" % (args.seeds - 1, CONFIG_DESC["C2"]), "gap_tol": 1e-6,
+                             "node_tol": 1e-8, "batch": args.batch, "runs": []}
+                for ext in (False, True):
+                    ts, ns = [], []
+                    for sd in range(args.seeds):
+                        inst2, _ = load_instance("C2", sd)
+                        rho2 = float(np.mean(np.einsum("ij,ij->j", inst2.X, inst2.X))) * args.rho_mult
+                        pr2 = Problem(np.asfortranarray(inst2.X), inst2.y, inst2.lambda0, inst2.lambda2, inst2.M,
+                                      rho=rho2, node_tol=1e-8, max_iters=10000, device=local)
+                        kw = dict(gap_tol=1e-6, batch=args.batch, init_mp=ext, early_prune=ext, time_limit_s=60.0)
+                        pr2.l0l2_solve(**kw)   # warm-up
+                        torch.cuda.synchronize(dev)
+                        t = time.perf_counter()
+                        r2 = pr2.l0l2_solve(**kw)
+                        dt2 = time.perf_counter() - t
+                        pr2.close()
+                        if r2["stats"]["status"] <= 1:
+                            ts.append(dt2)
+                        ns.append(r2["stats"]["nodes"])
+                    q = np.percentile(ts, [25, 50, 75]) if ts else [None] * 3
+                    seeds_blk["runs"].append({"init_mp": ext, "early_prune": ext, "certified": len(ts),
+                                              "time_s_median": q[1], "time_s_iqr": [q[0], q[2]],
+                                              "nodes_median": float(np.median(ns)), "times_s": ts, "nodes": ns})
+                certified.append(seeds_blk)
+    except Exception as e:   # context sections never cost the headline line
+        section_errors['certified'] = repr(e)
 
     # C5 (n = 500, p = 2e4 Toeplitz 0.9, SNR 1) along the paper's λ0 path (P:883 multipliers), each solve
     # time-limited: the gap reached at the limit
     c5sweep = None
-    if world == 1 and not args.no_certified and args.c5_time_limit > 0:
-        import synth
-        c5sweep = {"workload": "C5 seed %d: %s, lambda0 = m * lambda0*, gap_tol 1e-2, node_tol 1e-4, time limit %g s"
-                               % (args.seed, CONFIG_DESC["C5"], args.c5_time_limit), "runs": []}
-        for mult in (0.05, 0.2, 0.4, 0.6, 1.5, 2.0):
-            inst5 = synth.config_instance("C5", seed=args.seed, lambda0_mult=mult)
-            rho5 = float(np.mean(np.einsum("ij,ij->j", inst5.X, inst5.X))) * args.rho_mult
-            pr5 = Problem(np.asfortranarray(inst5.X), inst5.y, inst5.lambda0, inst5.lambda2, inst5.M, rho=rho5,
-                          node_tol=1e-4, max_iters=10000, device=local)
-            torch.cuda.synchronize(dev)
-            t = time.perf_counter()
-            r5 = pr5.l0l2_solve(gap_tol=1e-2, batch=args.batch, init_mp=True, early_prune=True,
-                                time_limit_s=args.c5_time_limit)
-            dt5 = time.perf_counter() - t
-            st5 = r5["stats"]
-            pr5.close()
-            c5sweep["runs"].append({"lambda0_mult": mult, "lambda0": inst5.lambda0, "time_s": dt5,
-                                    "certified": st5["status"] <= 1, "gap": r5["gap"], "nodes": st5["nodes"],
-                                    "nodes_per_s": st5["nodes"] / dt5, "max_open": st5["max_open"],
-                                    "support_size": st5["support_size"], "objective": r5["obj"]})
+    try:
+        if world == 1 and not args.no_certified and args.c5_time_limit > 0:
+            import synth
+            c5sweep = {"workload": "C5 seed %d: %s, lambda0 = m * lambda0*, gap_tol 1e-2, node_tol 1e-4, time limit %g s"
+                                   % (args.seed, CONFIG_DESC["C5"], args.c5_time_limit), "runs": []}
+            for mult in (0.05, 0.2, 0.4, 0.6, 1.5, 2.0):
+                inst5 = synth.config_instance("C5", seed=args.seed, lambda0_mult=mult)
+                rho5 = float(np.mean(np.einsum("ij,ij->j", inst5.X, inst5.X))) * args.rho_mult
+                pr5 = Problem(np.asfortranarray(inst5.X), inst5.y, inst5.lambda0, inst5.lambda2, inst5.M, rho=rho5,
+                              node_tol=1e-4, max_iters=10000, device=local)
+                torch.cuda.synchronize(dev)
+                t = time.perf_counter()
+                r5 = pr5.l0l2_solve(gap_tol=1e-2, batch=args.batch, init_mp=True, early_prune=True,
+                                    time_limit_s=args.c5_time_limit)
+                dt5 = time.perf_counter() - t
+                st5 = r5["stats"]
+                pr5.close()
+                c5sweep["runs"].append({"lambda0_mult": mult, "lambda0": inst5.lambda0, "time_s": dt5,
+                                        "certified": st5["status"] <= 1, "gap": r5["gap"], "nodes": st5["nodes"],
+                                        "nodes_per_s": st5["nodes"] / dt5, "max_open": st5["max_open"],
+                                        "support_size": st5["support_size"], "objective": r5["obj"]})
+    except Exception as e:   # context sections never cost the headline line
+        section_errors['c5sweep'] = repr(e)
 
     # time-to-certified-optimality at the full C4 size: the recipe's λ0* leaves a tree that does not
     # close in minutes; λ0 = 2·λ0* (one of the paper's λ0-path multipliers) certifies a 1% gap
     c4cert = None
-    if world == 1 and not args.no_certified and args.config == "C4":
-        import synth
-        inst4 = synth.config_instance("C4", seed=args.seed, lambda0_mult=2.0)
-        c4cert = {"workload": "C4 seed %d with lambda0 = 2 lambda0* (P:883 path multiplier): %s"
-                              % (args.seed, CONFIG_DESC["C4"]),
-                  "lambda0": inst4.lambda0, "gap_tol": 1e-2, "node_tol": args.node_tol, "runs": []}
-        for ext in (False, True):
-            pr4 = Problem(np.asfortranarray(inst4.X), inst4.y, inst4.lambda0, inst4.lambda2, inst4.M, rho=rho,
-                          node_tol=args.node_tol, max_iters=10000, device=local)
-            torch.cuda.synchronize(dev)
-            t = time.perf_counter()
-            r4 = pr4.l0l2_solve(gap_tol=1e-2, batch=args.batch, init_mp=ext, early_prune=ext, time_limit_s=150.0)
-            dt4 = time.perf_counter() - t
-            st4 = r4["stats"]
-            c4cert["runs"].append({"init_mp": ext, "early_prune": ext, "time_to_certified_optimality_s": dt4,
-                                   "certified": st4["status"] <= 1, "gap": r4["gap"], "nodes": st4["nodes"],
-                                   "nodes_per_s": st4["nodes"] / dt4, "node_iters": st4["node_iters"],
-                                   "objective": r4["obj"], "support": [int(j) for j in r4["support"]]})
-            pr4.close()
+    try:
+        if world == 1 and not args.no_certified and args.config == "C4":
+            import synth
+            inst4 = synth.config_instance("C4", seed=args.seed, lambda0_mult=2.0)
+            c4cert = {"workload": "C4 seed %d with lambda0 = 2 lambda0* (P:883 path multiplier): %s"
+                                  % (args.seed, CONFIG_DESC["C4"]),
+                      "lambda0": inst4.lambda0, "gap_tol": 1e-2, "node_tol": args.node_tol, "runs": []}
+            for ext in (False, True):
+                pr4 = Problem(np.asfortranarray(inst4.X), inst4.y, inst4.lambda0, inst4.lambda2, inst4.M, rho=rho,
+                              node_tol=args.node_tol, max_iters=10000, device=local)
+                torch.cuda.synchronize(dev)
+                t = time.perf_counter()
+                r4 = pr4.l0l2_solve(gap_tol=1e-2, batch=args.batch, init_mp=ext, early_prune=ext, time_limit_s=150.0)
+                dt4 = time.perf_counter() - t
+                st4 = r4["stats"]
+                c4cert["runs"].append({"init_mp": ext, "early_prune": ext, "time_to_certified_optimality_s": dt4,
+                                       "certified": st4["status"] <= 1, "gap": r4["gap"], "nodes": st4["nodes"],
+                                       "nodes_per_s": st4["nodes"] / dt4, "node_iters": st4["node_iters"],
+                                       "objective": r4["obj"], "support": [int(j) for j in r4["support"]]})
+                pr4.close()
+    except Exception as e:   # context sections never cost the headline line
+        section_errors['certified_c4'] = repr(e)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(inst, args, rho, args.cpu_seconds)
-        if args.oracle_bnb:
-            cpu["measured_bnb"] = oracle_bnb(args.oracle_bnb, args.seed, args.rho_mult, batch=args.batch)
+    try:
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(inst, args, rho, args.cpu_seconds)
+            if args.oracle_bnb:
+                cpu["measured_bnb"] = oracle_bnb(args.oracle_bnb, args.seed, args.rho_mult, batch=args.batch)
+    except Exception as e:   # context sections never cost the headline line
+        section_errors['cpu'] = repr(e)
     if rank == 0:
         st = last["stats"]
         line = {"metric": "BnB nodes/sec", "value": value, "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
@@ -624,6 +640,8 @@ def main():
                 "phase_s": {"bound": st["t_bound"], "upper": st["t_upper"], "tree": st["t_tree"], "comm": st["t_comm"]},
                 "create_s": t_create, "gpu_launches": int(launches), "device_bytes": int(info["device_bytes"]),
                 "roofline": roof, "upper_bound_kernel": upper, "e2e": e2e, "clocks": clk.summary()}
+        if section_errors:
+            line["section_errors"] = section_errors
         if certified is not None:
             line["certified_solves"] = certified
         if micro is not None:
@@ -633,16 +651,22 @@ def main():
         if c4cert is not None:
             line["certified_c4"] = c4cert
         ttc = {}
-        if c4cert is not None:
-            for r in c4cert["runs"]:
-                if r["certified"]:
-                    ttc["C4 lambda0=2*lambda0* gap 1e-2%s" % (" +MP+early prune" if r["init_mp"] else "")] = \
-                        r["time_to_certified_optimality_s"]
-        for blk in (certified or []):
-            for r in blk["runs"]:
-                if r["certified"]:
-                    ttc["%s gap %g%s" % (blk["workload"].split()[0], r["gap_tol"], " +MP+early prune" if r["init_mp"]
-                                         else "")] = r["time_to_certified_optimality_s"]
+        try:
+            if c4cert is not None:
+                for r in c4cert["runs"]:
+                    if r["certified"]:
+                        ttc["C4 lambda0=2*lambda0* gap 1e-2%s" % (" +MP+early prune" if r["init_mp"] else "")] = \
+                            r["time_to_certified_optimality_s"]
+            for blk in (certified or []):
+                for r in blk["runs"]:
+                    if "time_to_certified_optimality_s" in r and r["certified"]:
+                        ttc["%s gap %g%s" % (blk["workload"].split()[0], r["gap_tol"], " +MP+early prune" if r["init_mp"]
+                                             else "")] = r["time_to_certified_optimality_s"]
+                    elif "time_s_median" in r and r["time_s_median"] is not None:   # the C2 seeds block
+                        ttc["C2 seeds 0-%d median gap %g%s" % (args.seeds - 1, blk["gap_tol"], " +MP+early prune"
+                                                                if r["init_mp"] else "")] = r["time_s_median"]
+        except Exception as e:
+            line.setdefault("section_errors", {})["time_to_certified_optimality"] = repr(e)
         line["time_to_certified_optimality"] = {"unit": "s", "runs": ttc,
                                                 "note": "wall time of l0l2_solve to a certified gap, X resident, per "
                                                         "instance (key = config, lambda0, gap_tol, options)"}

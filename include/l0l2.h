@@ -228,6 +228,36 @@ typedef struct {
 } l0l2_transport;
 int l0l2_comm_init_transport(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const l0l2_transport* t);
 
+/*
+ * Column-sharded single-node ADMM for the narrow-frontier phases of a tree (the
+ * root, the ramp-up, narrow C2/C3-class trees), where node parallelism leaves GPUs idle.  Rank `rank`
+ * of `nranks` holds columns [col0, col0 + p_r) of the n × p_total design matrix (X_r: n × p_r
+ * column-major, host pointer; y: the full n-vector on every rank).  l0l2_create_sharded runs the
+ * tree-wide precompute with A = Σ_r X_r X_rᵀ + ρI all-reduced over the ranks (ρ = 0 → the
+ * mean of ‖X_j‖² over ALL columns) and keeps Z_r = L⁻¹X_r; the communicator is the caller's host
+ * transport `t` (several ranks may share one GPU) or, if t is NULL, NCCL from `nccl_id` (one GPU per
+ * rank).  Collective: every rank calls it.  The direct regime is not used (always the Z-form).
+ * Errors: as l0l2_create, plus L0L2_EINVAL for inconsistent shard arguments, L0L2_ENCCL.
+ */
+int l0l2_create_sharded(const double* X_r, const double* y, int64_t n, int64_t p_r, int64_t col0, int64_t p_total,
+                        double lambda0, double lambda2, const l0l2_opts* opts, int32_t nranks, int32_t rank,
+                        const l0l2_transport* t, const uint8_t nccl_id[128], l0l2_ctx** out);
+
+/*
+ * l0l2_bound_sharded — the lower bounds of B ≤ 128 nodes (the semantics of l0l2_bound_batch: ADMM
+ * on eq:ADMM1, warm starts P:543, dual of Proposition 1 and primal every check_every iterations, stop
+ * at node_tol) computed by ALL ranks of a sharded context together: per iteration u = Σ_r Z_r w_r is
+ * all-reduced (n × B doubles) and each rank updates its own columns; at checks the per-node dual /
+ * primal terms and X_r β are all-reduced once.  Collective.  DEVICE pointers on `stream`:
+ *   fix_off int64[B+1], fix_idx int32 (GLOBAL column indices; each rank applies its own), fix_val;
+ *   warm_in double[B][2][p_r] (this rank's columns of (β, v)) or NULL (cold); parent_lb double[B] or NULL;
+ *   out lb[B], primal[B], iters[B], flags[B] (identical on every rank), warm_out[B][2][p_r] or NULL.
+ * Returns L0L2_WNOTCONV if a node stopped at max_iters.
+ */
+int l0l2_bound_sharded(l0l2_ctx* ctx, int32_t B, const int64_t* fix_off, const int32_t* fix_idx,
+                       const uint8_t* fix_val, const double* warm_in, const double* parent_lb, double* lb,
+                       double* primal, double* warm_out, int32_t* iters, uint8_t* flags, void* stream);
+
 /* Frontier rebalancing plan used by l0l2_solve every rebalance_every rounds (pure host logic,
  * exported for tests).  counts[r] = open nodes on rank r.  While the emptiest rank holds fewer
  * than `batch` nodes and the fullest holds ≥ 2 more, move half the difference (ties → lowest

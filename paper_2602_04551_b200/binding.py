@@ -102,6 +102,11 @@ def load_library():
     lib.l0l2_kernel_stats.restype = C.c_int
     lib.l0l2_solve_trace.argtypes = [P, P, C.c_int64]
     lib.l0l2_solve_trace.restype = C.c_int64
+    lib.l0l2_create_sharded.argtypes = [P, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double,
+                                        C.POINTER(_Opts), C.c_int32, C.c_int32, P, P, C.POINTER(P)]
+    lib.l0l2_create_sharded.restype = C.c_int
+    lib.l0l2_bound_sharded.argtypes = [P, C.c_int32] + [P] * 10 + [P]
+    lib.l0l2_bound_sharded.restype = C.c_int
     lib.l0l2_info.argtypes = [P] + [P] * 5
     lib.l0l2_info.restype = C.c_int
     lib.l0l2_last_error.argtypes = [P]
@@ -398,3 +403,70 @@ class Problem:
                                  branch_j=int(r[5]), flags=int(r[6]), ub=r[7], parent=int(r[8]), lastfix=int(r[9]))
                             for r in buf[:nrec]]
         return out
+
+
+class ShardedProblem:
+    """Column-sharded context (l0l2_create_sharded): this rank's columns [col0, col0 + p_r) of X;
+    the current torch.distributed group carries the exchange (transport "host": the library's host
+    transport over the group, ranks may share a GPU; "nccl": one GPU per rank).  Marshalling only."""
+
+    def __init__(self, X_r, y, col0, p_total, lambda0, lambda2, M, rho=0.0, node_tol=1e-4, int_tol=1e-4,
+                 check_every=10, max_iters=10000, device=0, transport="host"):
+        import torch.distributed as dist
+        self._lib = load_library()
+        o = _Opts()
+        self._lib.l0l2_default_opts(C.byref(o))
+        o.M, o.rho, o.node_tol, o.int_tol = float(M), float(rho), float(node_tol), float(int_tol)
+        o.check_every, o.max_iters, o.device = int(check_every), int(max_iters), int(device)
+        Xf = np.asfortranarray(X_r, dtype=np.float64)
+        yf = np.ascontiguousarray(y, dtype=np.float64)
+        self.n, self.p = Xf.shape
+        self.col0, self.p_total = int(col0), int(p_total)
+        W, R = (dist.get_world_size(), dist.get_rank()) if dist.is_initialized() else (1, 0)
+        self._transport, uid = None, None
+        if W > 1 and transport == "host":
+            self._transport = HostTransport()
+        elif W > 1:
+            obj = [nccl_unique_id() if R == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        ctx = P()
+        rc = self._lib.l0l2_create_sharded(Xf.ctypes.data, yf.ctypes.data, self.n, self.p, self.col0, self.p_total,
+                                           float(lambda0), float(lambda2), C.byref(o), W, R,
+                                           C.byref(self._transport.struct) if self._transport else None,
+                                           C.cast(uid, P) if uid is not None else None, C.byref(ctx))
+        if rc != OK:
+            raise L0L2Error(rc, self._lib.l0l2_last_error(None).decode(errors="replace"))
+        self._ctx = ctx
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self._lib.l0l2_destroy(self._ctx)
+            self._ctx = None
+
+    def l0l2_bound_sharded(self, fixings, warm_in=None, parent_lb=None):
+        """fixings: list of (F0, F1) with GLOBAL column indices; warm_in: torch CUDA [B, 2, p_r] or None."""
+        import torch
+        dev = torch.device("cuda", torch.cuda.current_device())
+        B = len(fixings)
+        off, idx, val = [0], [], []
+        for F0, F1 in fixings:
+            idx += [int(j) for j in F0] + [int(j) for j in F1]
+            val += [0] * len(F0) + [1] * len(F1)
+            off.append(len(idx))
+        t_off = torch.tensor(off, dtype=torch.int64, device=dev)
+        t_idx = torch.tensor(idx or [0], dtype=torch.int32, device=dev)
+        t_val = torch.tensor(val or [0], dtype=torch.uint8, device=dev)
+        plb = torch.tensor(parent_lb, dtype=torch.float64, device=dev) if parent_lb is not None else None
+        lb = torch.empty(B, dtype=torch.float64, device=dev)
+        primal = torch.empty_like(lb)
+        wout = torch.empty((B, 2, self.p), dtype=torch.float64, device=dev)
+        iters = torch.empty(B, dtype=torch.int32, device=dev)
+        flags = torch.empty(B, dtype=torch.uint8, device=dev)
+        win = warm_in.contiguous() if warm_in is not None else None
+        torch.cuda.current_stream().synchronize()
+        rc = self._lib.l0l2_bound_sharded(self._ctx, B, _ptr(t_off), _ptr(t_idx), _ptr(t_val), _ptr(win), _ptr(plb),
+                                          _ptr(lb), _ptr(primal), _ptr(wout), _ptr(iters), _ptr(flags), None)
+        _check(rc, self._ctx)
+        torch.cuda.synchronize()
+        return dict(lb=lb, primal=primal, warm_out=wout, iters=iters, flags=flags, rc=rc)

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libl0l2.so")
-SOURCES = ["gemm.cu", "precompute.cu", "admm.cu", "upper.cu", "mp.cu", "capi.cu", "solve.cu", "frontier.cu"]
+SOURCES = ["gemm.cu", "precompute.cu", "admm.cu", "upper.cu", "mp.cu", "capi.cu", "solve.cu", "frontier.cu", "sharded.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -77,6 +77,7 @@ void l0l2_destroy(l0l2_ctx* ctx) {
   for (void* s : c->scr) if (s) cudaFree(s);
   for (double* m : c->pool_chunks) cudaFree(m);
   if (c->solve_buf) cudaFree(c->solve_buf);
+  if (c->sh_buf) cudaFree(c->sh_buf);
   if (c->solve_stream) cudaStreamDestroy(c->solve_stream);
   for (auto e : c->ev) if (e) cudaEventDestroy(e);
   comm_free(c);
@@ -84,8 +85,18 @@ void l0l2_destroy(l0l2_ctx* ctx) {
   delete ctx;
 }
 
-int l0l2_create(const double* X, const double* y, int64_t n, int64_t p, double lambda0, double lambda2,
-                const l0l2_opts* opts, l0l2_ctx** out) {
+}  // extern "C"
+
+namespace {
+struct ShardCfg {   // column-sharded context (sharded.cu): this rank's columns and its communicator
+  int64_t col0, p_total;
+  int32_t nranks, rank;
+  const l0l2_transport* t;
+  const uint8_t* nccl_id;
+};
+
+int create_impl(const double* X, const double* y, int64_t n, int64_t p, double lambda0, double lambda2,
+                const l0l2_opts* opts, const ShardCfg* sh, l0l2_ctx** out) {
   if (out) *out = nullptr;
   auto fail = [](int code, const char* msg) {
     g_last_error = msg;
@@ -118,6 +129,11 @@ int l0l2_create(const double* X, const double* y, int64_t n, int64_t p, double l
   c->int_tol = opts->int_tol;
   c->check_every = opts->check_every;
   c->max_iters = opts->max_iters;
+  if (sh) {
+    c->sharded = 1;
+    c->col0 = sh->col0;
+    c->p_total = sh->p_total;
+  }
   int rc = L0L2_OK;
   auto bail = [&](int code) {
     g_last_error = c->err;
@@ -178,10 +194,20 @@ int l0l2_create(const double* X, const double* y, int64_t n, int64_t p, double l
     c->ldD = padded_ld(c->p);
     c->direct = (c->p <= 2 * c->n && c->ldD <= padded_ld(1056)) ? 1 : 0;
     if (const char* e = getenv("L0L2_DIRECT")) c->direct = c->direct && atoi(e) != 0;   // test / tuning hook
-    rc = precompute(c, st);
-    ok = rc == L0L2_OK;
+    if (sh) {   // the sharded precompute all-reduces XXᵀ over the ranks (Z-form only)
+      c->direct = 0;
+      if (sh->nranks > 1) {
+        rc = sh->t ? l0l2_comm_init_transport(ctx, sh->nranks, sh->rank, sh->t)
+                   : l0l2_comm_init(ctx, sh->nranks, sh->rank, sh->nccl_id);
+        ok = rc == L0L2_OK;
+      }
+    }
+    if (ok) {
+      rc = precompute(c, st);
+      ok = rc == L0L2_OK;
+    }
   }
-  if (ok) {
+  if (ok && !sh) {   // the fused node-parallel kernel (a sharded context runs sharded.cu's loop)
     rc = admm_alloc(c);
     ok = rc == L0L2_OK;
   }
@@ -190,6 +216,42 @@ int l0l2_create(const double* X, const double* y, int64_t n, int64_t p, double l
   if (!ok) return bail(rc ? rc : L0L2_ECUDA);
   *out = ctx;
   return L0L2_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int l0l2_create(const double* X, const double* y, int64_t n, int64_t p, double lambda0, double lambda2,
+                const l0l2_opts* opts, l0l2_ctx** out) {
+  return create_impl(X, y, n, p, lambda0, lambda2, opts, nullptr, out);
+}
+
+int l0l2_create_sharded(const double* X_r, const double* y, int64_t n, int64_t p_r, int64_t col0, int64_t p_total,
+                        double lambda0, double lambda2, const l0l2_opts* opts, int32_t nranks, int32_t rank,
+                        const l0l2_transport* t, const uint8_t nccl_id[128], l0l2_ctx** out) {
+  if (out) *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks || col0 < 0 || p_r <= 0 || col0 + p_r > p_total ||
+      (nranks > 1 && !t && !nccl_id)) {
+    g_last_error = "l0l2_create_sharded: bad shard / communicator arguments";
+    return L0L2_EINVAL;
+  }
+  const ShardCfg sh{col0, p_total, nranks, rank, t, nccl_id};
+  return create_impl(X_r, y, n, p_r, lambda0, lambda2, opts, &sh, out);
+}
+
+int l0l2_bound_sharded(l0l2_ctx* ctx, int32_t B, const int64_t* fix_off, const int32_t* fix_idx,
+                       const uint8_t* fix_val, const double* warm_in, const double* parent_lb, double* lb,
+                       double* primal, double* warm_out, int32_t* iters, uint8_t* flags, void* stream) {
+  if (!ctx) return L0L2_EINVAL;
+  Ctx* c = &ctx->impl;
+  if (!c->sharded) return set_err(c, L0L2_EINVAL, "not a column-sharded context (l0l2_create_sharded)");
+  if (B < 0 || B > 128) return set_err(c, L0L2_EINVAL, "0 <= B <= 128");
+  if (B == 0) return L0L2_OK;
+  if (!lb || !primal || !iters || !flags) return set_err(c, L0L2_EINVAL, "null output");
+  L0L2_CUDA(c, cudaSetDevice(c->device));
+  return bound_sharded(c, B, fix_off, fix_idx, fix_val, warm_in, parent_lb, lb, primal, warm_out, iters, flags,
+                       (cudaStream_t)stream);
 }
 
 int l0l2_info(const l0l2_ctx* ctx, int64_t* n, int64_t* p, double* rho, int64_t* device_bytes, int64_t* launches) {

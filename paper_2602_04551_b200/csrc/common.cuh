@@ -112,6 +112,11 @@ struct Ctx {
   cudaStream_t solve_stream = nullptr;
   size_t pool_cap = 0;
   void* fr_state = nullptr;   // device frontier arrays (frontier.cu), kept across solves
+  // column-sharded single-node ADMM (sharded.cu): this rank holds columns [col0, col0 + p) of p_total
+  int sharded = 0;
+  int64_t col0 = 0, p_total = 0;
+  void* sh_buf = nullptr;
+  size_t sh_bytes = 0;
 };
 
 int set_err(Ctx* c, int code, const char* fmt, ...);
@@ -189,6 +194,10 @@ int mp_run(Ctx* c, int max_rounds, cudaStream_t st, std::vector<int32_t>& S_out,
            double* obj, int* rounds);
 
 void comm_free(Ctx* c);
+int shard_allreduce(Ctx* c, double* d, int64_t count, cudaStream_t st);   // solve.cu
+int bound_sharded(Ctx* c, int B, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
+                  const double* warm_in, const double* parent_lb, double* lb, double* primal, double* warm_out,
+                  int32_t* iters, uint8_t* flags, cudaStream_t st);   // sharded.cu
 
 }  // namespace l0l2
 

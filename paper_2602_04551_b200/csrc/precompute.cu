@@ -158,10 +158,14 @@ int precompute(Ctx* c, cudaStream_t st) {
     if (!d_rho) return set_err(c, L0L2_ENOMEM, "rho scratch");
     sum_vec<<<1, 256, 0, st>>>(c->colsq, p, d_rho);
     L0L2_LAUNCHED(c);
+    if (c->sharded) {   // the mean over ALL columns (column-sharded context, sharded.cu)
+      int rc0 = shard_allreduce(c, d_rho, 1, st);
+      if (rc0) return rc0;
+    }
     double s = 0.0;
     L0L2_CUDA(c, cudaMemcpyAsync(&s, d_rho, sizeof(double), cudaMemcpyDeviceToHost, st));
     L0L2_CUDA(c, cudaStreamSynchronize(st));
-    c->rho = s / (double)p;
+    c->rho = s / (double)(c->sharded ? c->p_total : p);
   }
   L0L2_CUDA(c, cudaFuncSetAttribute(potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotrfSmem));
   L0L2_CUDA(c, cudaMemsetAsync(info, 0, sizeof(int), st));
@@ -170,6 +174,8 @@ int precompute(Ctx* c, cudaStream_t st) {
   // A = X Xᵀ + ρ I  (op(B) = Xᵀ: element (k, col) = X[col + k*ld])
   int rc = gemm_f64(c, n, n, p, 1.0, c->X, ld, false, c->X, ld, true, 0.0, A, ld, st);
   if (rc) return rc;
+  // column-sharded context: A = Σ_r X_r X_rᵀ over the ranks' columns (sharded.cu)
+  if (c->sharded && (rc = shard_allreduce(c, A, ld * n, st))) return rc;
   add_diag<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A, ld, n, c->rho);
   L0L2_LAUNCHED(c);
   // Z starts as a copy of X (padded rows / columns are zero)

@@ -31,6 +31,7 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -57,6 +58,7 @@ static NcclApi* load_nccl(std::string& err) {
   SYM("ncclGetUniqueId", GetUniqueId)
   SYM("ncclCommInitRank", CommInitRank)
   SYM("ncclAllGather", AllGather)
+  SYM("ncclAllReduce", AllReduce)
   SYM("ncclBroadcast", Broadcast)
   SYM("ncclSend", Send)
   SYM("ncclRecv", Recv)
@@ -67,6 +69,34 @@ static NcclApi* load_nccl(std::string& err) {
 #undef SYM
   ok = true;
   return &api;
+}
+
+// Sum of a device vector over the ranks, identical on every rank (column-sharded ADMM, sharded.cu;
+// the sharded precompute): NCCL all-reduce on the stream, or over the host transport an all-gather
+// and a sum in rank order on the host.
+int shard_allreduce(Ctx* c, double* d, int64_t count, cudaStream_t st) {
+  if (c->nranks <= 1 || count <= 0) return L0L2_OK;
+  if (c->host_tr_set) {
+    const size_t bytes = sizeof(double) * (size_t)count;
+    std::vector<double> mine((size_t)count), all((size_t)count * c->nranks);
+    L0L2_CUDA(c, cudaMemcpyAsync(mine.data(), d, bytes, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    const l0l2_transport& t = c->host_tr;
+    if (t.allgather(t.user, mine.data(), all.data(), (int64_t)bytes))
+      return set_err(c, L0L2_ENCCL, "host transport allgather failed");
+    for (int64_t i = 0; i < count; i++) {
+      double a = all[(size_t)i];
+      for (int r = 1; r < c->nranks; r++) a += all[(size_t)r * count + i];
+      mine[(size_t)i] = a;
+    }
+    L0L2_CUDA(c, cudaMemcpyAsync(d, mine.data(), bytes, cudaMemcpyHostToDevice, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    return L0L2_OK;
+  }
+  if (!c->nccl || !c->nccl_comm) return set_err(c, L0L2_ENCCL, "communicator not initialised");
+  ncclResult_t r = c->nccl->AllReduce(d, d, (size_t)count, ncclDouble, ncclSum, (ncclComm_t)c->nccl_comm, st);
+  if (r != ncclSuccess) return set_err(c, L0L2_ENCCL, "ncclAllReduce: %s", c->nccl->GetErrorString(r));
+  return L0L2_OK;
 }
 
 void comm_free(Ctx* c) {
