@@ -78,6 +78,7 @@ void l0l2_destroy(l0l2_ctx* ctx) {
   for (double* m : c->pool_chunks) cudaFree(m);
   if (c->solve_buf) cudaFree(c->solve_buf);
   if (c->sh_buf) cudaFree(c->sh_buf);
+  if (c->gemm_ws) cudaFree(c->gemm_ws);
   if (c->solve_stream) cudaStreamDestroy(c->solve_stream);
   for (auto e : c->ev) if (e) cudaEventDestroy(e);
   comm_free(c);

@@ -117,6 +117,8 @@ struct Ctx {
   int64_t col0 = 0, p_total = 0;
   void* sh_buf = nullptr;
   size_t sh_bytes = 0;
+  void* gemm_ws = nullptr;    // split-K partials of gemm_f64
+  size_t gemm_ws_bytes = 0;
 };
 
 int set_err(Ctx* c, int code, const char* fmt, ...);

@@ -2,6 +2,8 @@
 // tcgen05 has no f64 kind, so FP64 contractions use warp-level DMMA
 // with register accumulators.  Used by the tree-wide precompute (A = XXᵀ+ρI,
 // blocked Cholesky trailing updates, Z = L⁻¹X) and by the optional r̂ = y − Xb̂ output.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace l0l2 {
@@ -18,7 +20,11 @@ template <bool TA, bool TB>
 __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t K, double alpha,
                                                    const double* __restrict__ A, int64_t lda,
                                                    const double* __restrict__ B, int64_t ldb,
-                                                   double beta, double* __restrict__ C, int64_t ldc) {
+                                                   double beta, double* __restrict__ C, int64_t ldc,
+                                                   int64_t ksplit, int64_t zstride) {
+  // split-K (blockIdx.z): this CTA's K range [kb, ke); its partial goes to C + z·zstride
+  const int64_t kb = (int64_t)blockIdx.z * ksplit, ke = min(K, kb + ksplit);
+  C += (int64_t)blockIdx.z * zstride;
   __shared__ double As[2][BK][PADS];
   __shared__ double Bs[2][BK][PADS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -40,14 +46,14 @@ __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t
       if (!TA) { mm = e & 63; kk = e >> 6; } else { kk = e & 15; mm = e >> 4; }
       int64_t gm = m0 + mm, gk = k0 + kk;
       double v = 0.0;
-      if (gm < M && gk < K) v = TA ? A[gk + gm * lda] : A[gm + gk * lda];
+      if (gm < M && gk < ke) v = TA ? A[gk + gm * lda] : A[gm + gk * lda];
       ra[r] = v;
       int nn;
       if (!TB) { kk = e & 15; nn = e >> 4; } else { nn = e & 63; kk = e >> 6; }
       int64_t gn = n0 + nn;
       gk = k0 + kk;
       v = 0.0;
-      if (gn < N && gk < K) v = TB ? B[gn + gk * ldb] : B[gk + gn * ldb];
+      if (gn < N && gk < ke) v = TB ? B[gn + gk * ldb] : B[gk + gn * ldb];
       rb[r] = v;
     }
   };
@@ -63,13 +69,13 @@ __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t
       Bs[buf][kk][nn] = rb[r];
     }
   };
-  const int64_t nk = (K + BK - 1) / BK;
-  gload(0);
+  const int64_t nk = ke > kb ? (ke - kb + BK - 1) / BK : 0;
+  if (nk > 0) gload(kb);
   sstore(0);
   __syncthreads();
   for (int64_t kt = 0; kt < nk; kt++) {
     const int buf = kt & 1;
-    if (kt + 1 < nk) gload((kt + 1) * BK);
+    if (kt + 1 < nk) gload(kb + (kt + 1) * BK);
 #pragma unroll
     for (int ks = 0; ks < BK; ks += 4) {
       double af[4], bf[2];
@@ -100,6 +106,18 @@ __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t
       }
 }
 
+// split-K epilogue: C = alpha·Σ_z part[z] + beta·C, the partials summed in z order (deterministic)
+__global__ void splitk_reduce(int64_t M, int64_t N, int splits, const double* __restrict__ part, double alpha,
+                              double beta, double* __restrict__ C, int64_t ldc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M * N) return;
+  const int64_t m = e % M, n = e / M;
+  double a = 0.0;
+  for (int z = 0; z < splits; z++) a += part[(int64_t)z * M * N + e];
+  double* cp = C + m + n * ldc;
+  *cp = alpha * a + (beta == 0.0 ? 0.0 : beta * *cp);
+}
+
 }  // namespace
 
 int gemm_f64(Ctx* c, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
@@ -108,11 +126,42 @@ int gemm_f64(Ctx* c, int64_t M, int64_t N, int64_t K, double alpha, const double
   if (M <= 0 || N <= 0) return L0L2_OK;
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
   if (grid.y > 65535) return set_err(c, L0L2_EINVAL, "gemm: M too large");
-  if (!transA && !transB) gemm_kernel<false, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else if (!transA && transB) gemm_kernel<false, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else if (transA && !transB) gemm_kernel<true, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else gemm_kernel<true, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  // few output tiles and a long K (e.g. u = Z w: n × B × p): split K over ~2 CTAs per SM, partials
+  // to a workspace, then a fixed-order sum
+  const int64_t tiles = (int64_t)grid.x * grid.y;
+  int splits = 1;
+  if (tiles < c->sms && K >= 8 * BK * 16)
+    splits = (int)std::min<int64_t>({(2 * c->sms + tiles - 1) / tiles, K / (BK * 16), 128});
+  const int64_t ksplit = splits > 1 ? ((K + splits - 1) / splits + BK - 1) / BK * BK : K;
+  if (splits > 1) splits = (int)((K + ksplit - 1) / ksplit);
+  double* Cout = C;
+  int64_t ldo = ldc, zstride = 0;
+  double a_out = alpha, b_out = beta;
+  if (splits > 1) {
+    const size_t need = sizeof(double) * (size_t)splits * M * N;
+    if (c->gemm_ws_bytes < need) {
+      if (c->gemm_ws) cudaFree(c->gemm_ws);
+      c->gemm_ws = nullptr;
+      c->gemm_ws_bytes = 0;
+      if (cudaMalloc(&c->gemm_ws, need) != cudaSuccess) { cudaGetLastError(); return set_err(c, L0L2_ENOMEM, "gemm split-K"); }
+      c->gemm_ws_bytes = need;
+    }
+    Cout = (double*)c->gemm_ws;
+    ldo = M;
+    zstride = M * N;
+    a_out = 1.0;
+    b_out = 0.0;
+    grid.z = (unsigned)splits;
+  }
+  if (!transA && !transB) gemm_kernel<false, false><<<grid, 256, 0, st>>>(M, N, K, a_out, A, lda, B, ldb, b_out, Cout, ldo, ksplit, zstride);
+  else if (!transA && transB) gemm_kernel<false, true><<<grid, 256, 0, st>>>(M, N, K, a_out, A, lda, B, ldb, b_out, Cout, ldo, ksplit, zstride);
+  else if (transA && !transB) gemm_kernel<true, false><<<grid, 256, 0, st>>>(M, N, K, a_out, A, lda, B, ldb, b_out, Cout, ldo, ksplit, zstride);
+  else gemm_kernel<true, true><<<grid, 256, 0, st>>>(M, N, K, a_out, A, lda, B, ldb, b_out, Cout, ldo, ksplit, zstride);
   L0L2_LAUNCHED(c);
+  if (splits > 1) {
+    splitk_reduce<<<(unsigned)((M * N + 255) / 256), 256, 0, st>>>(M, N, splits, Cout, alpha, beta, C, ldc);
+    L0L2_LAUNCHED(c);
+  }
   return L0L2_OK;
 }
 
