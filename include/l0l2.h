@@ -115,7 +115,8 @@ int l0l2_bound_batch(l0l2_ctx* ctx, int32_t B,
  * eq:upperboundbeta U_S(β) = ½‖y − X_Sβ‖² + λ2‖β‖² s.t. |β_i| ≤ M by the fast proximal
  * gradient method with Nesterov extrapolation t/(t+3) and Armijo backtracking
  * (eq:fpg_extrapolate..eq:fpg_armijo), batched one CTA per support (Gram
- * Q = X_SᵀX_S + 2λ2I by a multi-warp pre-pass, then the iterations in support space).
+ * Q = X_SᵀX_S + 2λ2I by a multi-warp pre-pass — or, for supports too large for shared memory
+ * (|S| ≳ 670, up to ~4000), by a gather + DMMA GEMM into HBM — then the iterations in support space).
  * DEVICE pointers, ordered on `stream`:
  *   in  supp_off int64[B+1], supp_idx int32[nnz]
  *   out obj      double[B]     U_S(β) + λ0|S|  (objective of eq:perspective at z = 1_S)

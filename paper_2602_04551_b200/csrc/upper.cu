@@ -267,6 +267,18 @@ __global__ void __launch_bounds__(32) fpg_kernel(const double* __restrict__ X, i
     for (int a = lane; a < s; a += 32) beta_s[o0 + a] = bb[a];
 }
 
+// X_S of one support gathered densely (n × s, ld n) for the large-support Gram GEMM
+__global__ void gather_cols(const double* __restrict__ X, int64_t ld, int64_t n, const int32_t* __restrict__ S, int s,
+                            double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * s) return;
+  out[e] = X[(int64_t)S[e / n] * ld + e % n];
+}
+__global__ void add_diag_q(double* Q, int s, double v) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a < s) Q[(int64_t)a * s + a] += v;
+}
+
 }  // namespace
 
 int upper_batch(Ctx* c, int B, const int64_t* supp_off, const int32_t* supp_idx, double* obj, double* beta_s,
@@ -301,7 +313,43 @@ int upper_batch(Ctx* c, int B, const int64_t* supp_off, const int32_t* supp_idx,
       }
     }
     Qg = (double*)c->ub_scratch;
-    if (smem > limit) return set_err(c, L0L2_EINVAL, "support too large (%d)", smax);
+    if (smem > limit) {
+      // large supports (the vectors + staging no longer fit shared memory): the Gram of every support
+      // is formed in HBM by a gather + DMMA GEMM (Q = X_SᵀX_S + 2λ2I), and the FPG iterations run from
+      // it with only their six s-vectors in shared memory — the same iterates
+      const size_t vec6 = sizeof(double) * (size_t)6 * smax;
+      if (vec6 > limit) return set_err(c, L0L2_EINVAL, "support too large (%d)", smax);
+      double* XS = (double*)c->scratch_n(1, sizeof(double) * (size_t)c->n * smax);
+      if (!XS) return set_err(c, L0L2_ENOMEM, "upper-bound X_S scratch");
+      for (int k = 0; k < B; k++) {
+        const int sk = (int)(off[k + 1] - off[k]);
+        if (sk == 0) continue;
+        const int64_t tot = c->n * sk;
+        gather_cols<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->X, c->ld, c->n, supp_idx + off[k], sk, XS);
+        L0L2_LAUNCHED(c);
+        double* Qk = Qg + (int64_t)k * qstride;
+        int rc = gemm_f64(c, sk, sk, c->n, 1.0, XS, c->n, true, XS, c->n, false, 0.0, Qk, sk, st);
+        if (rc) return rc;
+        add_diag_q<<<(sk + 255) / 256, 256, 0, st>>>(Qk, sk, 2.0 * c->lam2);
+        L0L2_LAUNCHED(c);
+      }
+      L0L2_CUDA(c, cudaFuncSetAttribute(fpg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit));
+      if (!c->ev[2]) {
+        for (auto& e : c->ev) if (!e) L0L2_CUDA(c, cudaEventCreate(&e));
+      }
+      L0L2_CUDA(c, cudaEventRecord(c->ev[2], st));
+      fpg_kernel<<<B, 32, vec6, st>>>(c->X, c->ld, c->n, c->y, c->c, c->yy, c->lam0, c->lam2, c->M, supp_off, supp_idx,
+                                      obj, beta_s, nullptr, qstride, 0, 50000, Qg);
+      L0L2_LAUNCHED(c);
+      L0L2_CUDA(c, cudaEventRecord(c->ev[3], st));
+      L0L2_CUDA(c, cudaEventSynchronize(c->ev[3]));
+      float ms = 0.f;
+      L0L2_CUDA(c, cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
+      c->ks.upper_launches++;
+      c->ks.upper_ms += ms;
+      c->ks.upper_bytes_alg += 8.0 * (double)c->n * (double)(off[B] - off[0]);
+      return L0L2_OK;
+    }
   }
   // multi-warp Gram pre-pass when nw ≥ 2 warps' partials fit shared memory
   int gnw = 0;

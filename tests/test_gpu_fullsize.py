@@ -206,3 +206,21 @@ def test_c4_certified_solve_oracle_evidence():
     assert abs(res["obj"] - ref) <= 1e-9 * abs(ref), (res["obj"], ref)
     assert rel(res["beta"][res["support"]], bS) < 1e-6
     assert st["lb"] <= ref * (1 + 1e-12)
+
+
+def test_upper_bound_large_supports():
+    """Supports too large for the shared-memory FPG (|S| ≥ 670): the Gram is formed in HBM by a gather +
+    DMMA GEMM and the FPG iterations run from it; objective = the oracle's exact ridge on
+    the support (box inactive: M large), including |S| > n."""
+    inst = synth.make_instance(400, 3000, 5, 0.1, 3.0, 3)
+    lam0, lam2, M = 1.0, 2.0, 1e3
+    P = O.Problem(inst.X, inst.y, lam0, lam2, M)
+    rng = np.random.default_rng(5)
+    sups = [np.sort(rng.choice(inst.p, size=s, replace=False)) for s in (700, 1200, 5)]
+    prob = Problem(inst.X, inst.y, lam0, lam2, M)
+    obj, betas = prob.l0l2_upper_batch(sups)
+    prob.close()
+    for k, S in enumerate(sups):
+        ref, bS = O.upper_bound(P, S)
+        assert abs(float(obj[k]) - ref) <= 1e-9 * abs(ref), (len(S), float(obj[k]), ref)
+        assert rel(betas[k], bS) < 1e-6
