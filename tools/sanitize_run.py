@@ -46,6 +46,24 @@ def main(case):
         del os.environ["L0L2_NZCAP"]
         pr.l0l2_solve(gap_tol=1e-2, batch=16, node_limit=40, init_mp=True, early_prune=True)
         pr.close()
+    elif case == "round2":
+        # device frontier, continuous batching (host frontier), large-support upper bound, column-sharded bound
+        inst = synth.make_instance(80, 60, 5, 0.3, 3.0, 21)
+        lam2 = 0.5
+        lam0, M = synth.lambda0_rule(inst, lam2), synth.bigM_rule(inst, lam2)
+        pr = Problem(inst.X, inst.y, lam0, lam2, M, node_tol=1e-8)
+        pr.l0l2_solve(gap_tol=1e-4, batch=16, record=True, init_mp=True, early_prune=True)   # device frontier
+        pr.l0l2_solve(gap_tol=1e-4, batch=4, record=True, continuous=3)                      # host frontier
+        pr.close()
+        inst = synth.make_instance(200, 1500, 5, 0.1, 3.0, 3)
+        pr = Problem(inst.X, inst.y, 1.0, 2.0, 1e3)
+        rng = np.random.default_rng(1)
+        pr.l0l2_upper_batch([np.sort(rng.choice(inst.p, size=700, replace=False)), [0, 5, 9]])
+        pr.close()
+        from paper_2602_04551_b200 import ShardedProblem
+        sp = ShardedProblem(inst.X[:, :700], inst.y, 0, 700, 1.0, 2.0, 2.0, node_tol=1e-6, max_iters=300)
+        sp.l0l2_bound_sharded([((), ()), ((1,), (3,))])
+        sp.close()
     print("sanitize case %s done" % case)
 
 
