@@ -549,3 +549,37 @@ def test_early_prune_keeps_the_certificate(seed):
     early = [t for t in b["trace"] if t["early"]]
     assert all(t["pruned"] for t in early)          # an early-stopped node is always pruned
     assert not any(t["early"] for t in a["trace"])
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_mp_incumbent_keeps_the_certificate(seed):
+    """init_mp: the BnB started from Algorithm 3's incumbent (refit by the exact box ridge on
+    its support) certifies the brute-force optimum; its initial UB is the better of ½‖y‖², the MP point
+    and the refit, so the first round's threshold is never above the plain BnB's."""
+    inst = synth.make_instance(40, 12, 3, 0.3, 4.0, 30 + seed)
+    lam2 = max(synth.tune_lambda2(inst), 0.05)
+    P = O.Problem(inst.X, inst.y, synth.lambda0_rule(inst, lam2), lam2, synth.bigM_rule(inst, lam2))
+    bf_obj, bf_S, _ = O.brute_force(P)
+    r = O.bnb_solve(P, B=4, gap_tol=1e-9, node_tol=1e-9, record=True, init_mp=True)
+    assert r["obj"] == pytest.approx(bf_obj, rel=1e-9)
+    assert list(r["support"]) == list(bf_S)
+    mp = O.matching_pursuit(P)
+    ub0 = min(0.5 * P.yy, mp.obj, O.upper_bound(P, mp.support)[0] if len(mp.support) else np.inf)
+    assert r["trace"][0]["ub"] >= bf_obj * (1 - 1e-12)
+    assert ub0 >= bf_obj * (1 - 1e-12)                 # every incumbent is a feasible objective
+    plain = O.bnb_solve(P, B=4, gap_tol=1e-9, node_tol=1e-9)
+    assert r["nodes"] <= plain["nodes"]
+
+
+def test_node_map_does_not_change_the_tree():
+    """bnb_solve's node_map only decides where the independent nodes of a round run: a process pool
+    (the all-cores oracle baseline) gives the same tree, node for node, as the serial map."""
+    import multiprocessing as mp
+    inst = synth.make_instance(30, 10, 3, 0.2, 4.0, 7)
+    P = O.Problem(inst.X, inst.y, 1.0, 0.2, 3.0)
+    serial = O.bnb_solve(P, B=4, gap_tol=1e-9, node_tol=1e-9, record=True)
+    with mp.get_context("fork").Pool(2) as pool:
+        par = O.bnb_solve(P, B=4, gap_tol=1e-9, node_tol=1e-9, record=True, node_map=pool.map)
+    assert [(t["id"], t["lb"], t["iters"], t["branch_j"]) for t in serial["trace"]] == \
+        [(t["id"], t["lb"], t["iters"], t["branch_j"]) for t in par["trace"]]
+    assert serial["obj"] == par["obj"]
