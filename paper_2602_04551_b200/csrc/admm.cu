@@ -80,6 +80,14 @@ struct KP {
                                    // ≥ susp_min iterations in this launch) the launch suspends them (0 = off)
   int susp_min;
   double* out_lbbest;              // [nb] running max of checked duals (to resume a suspended node), or null
+  // step mode (column-sharded fused path, sharded.cu): the launch runs ONE phase and exits, the host
+  // all-reduces U (and at checks the per-node check totals and Zβ) across the ranks in between:
+  //   phase 0: u0 sweep (forward-only from w0) + reduction into U
+  //   phase 1: the warm refresh sweep + reduction
+  //   phase 2: one fused iteration + reduction; at a check also this rank's check totals (tot_out)
+  //            and Z_r β⁺ reduced into Ub (the decision runs in step_decide after the all-reduce)
+  int step_mode, step_phase, step_chk;
+  double* tot_out;                 // [kBC][4] this rank's Σ of the check terms (phase 2, check)
   int compact;                     // node-slot compaction allowed (tuning / test hook)
   int pfs;                         // tiles L2-prefetched by prefill (during the grid reduction)
   int tsplit;                      // bulk copies per Z tile (divides kPt)
@@ -949,6 +957,35 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k_in) {
   if (tid == 0) prefill(k, s, 0, false);
   __syncthreads();   // the sweep reads its node half and sub-ranges from s.sched
 
+  if (k.step_mode) {   // one phase per launch (column-sharded fused path, see KP)
+    if (k.step_phase == 0) {
+      sweep<SW_FWD_W, KS, MT, DIR>(k, s, false, false, phases, hph);
+    } else if (k.step_phase == 1) {
+      sweep<SW_FUSED, KS, MT, DIR>(k, s, true, false, phases, hph);
+    } else {
+      sweep<SW_FUSED, KS, MT, DIR>(k, s, false, k.step_chk != 0, phases, hph, k.sums);
+    }
+    grid_sync(k.bar);
+    reduce_u(k, s, k.U);
+    if (k.step_phase == 2 && k.step_chk) {
+      // this rank's totals of the check terms (sub-ranges in order) and Z_r β⁺ for ‖Xβ‖² = ‖L Σ_r Z_r β_r‖²
+      if (blockIdx.x == 0 && tid < kBC * 4) {
+        const int nd = tid >> 2, term = tid & 3;
+        double a = 0.0;
+        if (s.flags[nd] & F_ACTIVE)
+          for (int q = 0; q < k.nsr; q++) a += __ldcg(k.sums + ((int64_t)q * kBC + nd) * kSums + term);
+        k.tot_out[nd * 4 + term] = a;
+      }
+      grid_sync(k.bar);   // reduce_u has read Upart before the β sweep rewrites it
+      sweep<SW_FWD_BETA, KS, MT, DIR>(k, s, false, false, phases, hph);
+      grid_sync(k.bar);
+      reduce_u(k, s, k.Ub);
+    }
+    if (tid == 0)
+      for (int sg = 0; sg < NST && sg < s.sched[1]; sg++) mbar_wait(&s.mbar[sg], (phases >> sg) & 1u);
+    return;
+  }
+
   // u0 = Z (c + ρβ0 − v0), then the warm-start refresh sweep (R6: b, v of warm nodes; cold
   // nodes keep β = v = 0 and only their w⁺ = c is formed)
   sweep<SW_FWD_W, KS, MT, DIR>(k, s, false, false, phases, hph);
@@ -1259,6 +1296,48 @@ __global__ void fill_y(double* r, int64_t ldr, const double* y, int64_t n, int n
   r[(e / n) * ldr + e % n] = y[e % n];
 }
 
+// step mode decision (column-sharded fused path): from the ALL-REDUCED check totals and Zβ, per node
+// the dual of Proposition 1 at r̂ = y − X b̂, the primal with ‖Xβ‖² = ‖L Zβ‖²,
+// the running max (R7) and the stop rule (R8) — the same arithmetic as the in-kernel decision
+__global__ void step_decide(KP k, int it, const double* __restrict__ tot) {
+  const int nd = blockIdx.x;
+  int fl = k.nodei[nd * 2];
+  if (!(fl & F_ACTIVE)) return;
+  __shared__ double red[32];
+  double q = 0.0;
+  for (int64_t i = threadIdx.x; i < k.xn; i += blockDim.x) {   // (L Zβ)_i = Σ_{m ≤ i} L_im (Zβ)_m
+    const double* lrow = k.Lt + i * k.xld;
+    double a = 0.0;
+    for (int64_t m = 0; m <= i; m++) a = fma(lrow[m], k.Ub[nd * k.ld + m], a);
+    q = fma(a, a, q);
+  }
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = q;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double xx = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); w++) xx += red[w];
+  const double* T = tot + nd * 4;
+  const double dual = 0.5 * k.yy - 0.5 * T[0] - T[1];
+  const double primal = 0.5 * k.yy - T[2] + 0.5 * xx + T[3];
+  const double lbb = fmax(k.nodef[nd * 4 + 0], dual);
+  const int itn = k.nodei[nd * 2 + 1] + it;   // (it0 = 0 in step mode)
+  if ((primal - lbb) / fmax(1.0, fabs(primal)) <= k.node_tol) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_CONVERGED;
+  else if (it >= k.max_iters) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_MAXITER;
+  k.nodef[nd * 4 + 0] = lbb;
+  k.nodef[nd * 4 + 1] = primal;
+  k.nodef[nd * 4 + 3] = dual;
+  k.nodei[nd * 2 + 0] = fl;
+  k.out_iters[nd] = itn;   // iterations run so far (the node's count once it stops)
+}
+__global__ void step_outputs(KP k) {
+  const int nd = threadIdx.x;
+  if (nd >= k.nb) return;
+  k.out_lb[nd] = fmax(k.nodef[nd * 4 + 0], k.nodef[nd * 4 + 2]);
+  k.out_primal[nd] = k.nodef[nd * 4 + 1];
+  k.out_flags[nd] = (uint8_t)(k.nodei[nd * 2] & (L0L2_FLAG_CONVERGED | L0L2_FLAG_MAXITER));
+}
+
 using AdmmKernel = void (*)(KP);
 template <bool DIR>
 AdmmKernel admm_kernel_t(int cls) {
@@ -1416,10 +1495,53 @@ int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st) {
   return L0L2_OK;
 }
 
+KP make_kp(Ctx* c, const BoundArgs& a, unsigned mask);
+
 int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
   init_nodes<<<1, 32, 0, st>>>(a.nb, mask, a.cold_mask, a.parent_lb, a.lbbest_in, a.it0_in, a.warm_ptrs, c->node_f,
                                c->node_i);
   L0L2_LAUNCHED(c);
+  KP k = make_kp(c, a, mask);
+  void* args[] = {&k};
+  L0L2_CUDA(c, cudaLaunchCooperativeKernel((void*)admm_kernel(c->admm_cls, c->direct != 0), dim3(c->grid),
+                                           dim3(kAdmmThreads), args, admm_smem_bytes(k.ld), st));
+  L0L2_LAUNCHED(c);
+  return L0L2_OK;
+}
+
+// step mode launches (column-sharded fused path, sharded.cu): phase 0 initialises the group's nodes
+int admm_step(Ctx* c, const BoundArgs& a, int phase, int chk, double* tot_out, cudaStream_t st) {
+  const unsigned mask = (1u << a.nb) - 1u;
+  if (phase == 0) {
+    init_nodes<<<1, 32, 0, st>>>(a.nb, mask, a.cold_mask, a.parent_lb, nullptr, nullptr, nullptr, c->node_f, c->node_i);
+    L0L2_LAUNCHED(c);
+  }
+  KP k = make_kp(c, a, mask);
+  k.step_mode = 1;
+  k.step_phase = phase;
+  k.step_chk = chk;
+  k.tot_out = tot_out;
+  k.compact = 0;
+  void* args[] = {&k};
+  L0L2_CUDA(c, cudaLaunchCooperativeKernel((void*)admm_kernel(c->admm_cls, c->direct != 0), dim3(c->grid),
+                                           dim3(kAdmmThreads), args, admm_smem_bytes(k.ld), st));
+  L0L2_LAUNCHED(c);
+  return L0L2_OK;
+}
+int admm_step_decide(Ctx* c, const BoundArgs& a, int it, const double* tot, cudaStream_t st) {
+  KP k = make_kp(c, a, (1u << a.nb) - 1u);
+  step_decide<<<a.nb, 256, 0, st>>>(k, it, tot);
+  L0L2_LAUNCHED(c);
+  return L0L2_OK;
+}
+int admm_step_outputs(Ctx* c, const BoundArgs& a, cudaStream_t st) {
+  KP k = make_kp(c, a, (1u << a.nb) - 1u);
+  step_outputs<<<1, 32, 0, st>>>(k);
+  L0L2_LAUNCHED(c);
+  return L0L2_OK;
+}
+
+KP make_kp(Ctx* c, const BoundArgs& a, unsigned mask) {
   KP k{};
   k.act_mask = mask;
   k.prune_ub = a.prune_ub;
@@ -1466,11 +1588,7 @@ int launch_admm(Ctx* c, const BoundArgs& a, unsigned mask, cudaStream_t st) {
   k.a_4 = c->lam0 / (c->M * c->rho) + c->lam2 * c->M / c->rho;
   k.psi_l1 = 2.0 * std::sqrt(c->lam0 * c->lam2);
   k.psi_4 = c->lam0 / c->M + c->lam2 * c->M;
-  void* args[] = {&k};
-  L0L2_CUDA(c, cudaLaunchCooperativeKernel((void*)admm_kernel(c->admm_cls, c->direct != 0), dim3(c->grid), dim3(kAdmmThreads), args,
-                                           admm_smem_bytes(k.ld), st));
-  L0L2_LAUNCHED(c);
-  return L0L2_OK;
+  return k;
 }
 
 // Called after the stream has been synchronised past run_admm: accumulate the event-timed

@@ -208,9 +208,13 @@ int create_impl(const double* X, const double* y, int64_t n, int64_t p, double l
       ok = rc == L0L2_OK;
     }
   }
-  if (ok && !sh) {   // the fused node-parallel kernel (a sharded context runs sharded.cu's loop)
+  if (ok && !sh) {   // the fused node-parallel kernel
     rc = admm_alloc(c);
     ok = rc == L0L2_OK;
+  }
+  if (ok && sh) {    // a sharded context runs the same kernel in step mode on its shard when n fits
+    c->shard_fused = admm_alloc(c) == L0L2_OK ? 1 : 0;
+    c->err.clear();
   }
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);

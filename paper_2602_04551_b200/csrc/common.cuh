@@ -114,6 +114,7 @@ struct Ctx {
   void* fr_state = nullptr;   // device frontier arrays (frontier.cu), kept across solves
   // column-sharded single-node ADMM (sharded.cu): this rank holds columns [col0, col0 + p) of p_total
   int sharded = 0;
+  int shard_fused = 0;        // the fused step-mode kernel is available (n within the Z-form classes)
   int64_t col0 = 0, p_total = 0;
   void* sh_buf = nullptr;
   size_t sh_bytes = 0;
@@ -176,6 +177,10 @@ constexpr uint8_t kFlagSuspended = 16;   // node flag: suspended by continuous b
 int pack_group(Ctx* c, int nb, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
                const double* const* warm_ptrs_dev, cudaStream_t st);
 int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st);
+// step mode of the ADMM kernel (column-sharded fused path): one phase per launch (admm.cu)
+int admm_step(Ctx* c, const BoundArgs& a, int phase, int chk, double* tot_out, cudaStream_t st);
+int admm_step_decide(Ctx* c, const BoundArgs& a, int it, const double* tot, cudaStream_t st);
+int admm_step_outputs(Ctx* c, const BoundArgs& a, cudaStream_t st);
 int account_admm(Ctx* c, int nb, const int* iters_host);
 void account_admm_stats(Ctx* c, int nb, const int* iters_host, float ms);   // same, given the launch's time
 // device-frontier solve (frontier.cu): single rank, synchronous rounds

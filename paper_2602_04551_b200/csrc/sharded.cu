@@ -12,7 +12,9 @@
 // This is a host-stepped loop of library kernels (two GEMMs, an epilogue, a decision kernel per
 // iteration): unlike the fused persistent kernel it reads Z_r twice per iteration, and each
 // iteration pays one all-reduce latency — the price of splitting one node over W GPUs.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -183,10 +185,100 @@ __global__ void sh_init_nodes(int B, const double* warm_in_flag_src, uint8_t* ac
 
 }  // namespace
 
+// Fused variant: the persistent ADMM kernel on this rank's column shard in STEP mode (one phase per
+// launch: the u0 sweep, the refresh sweep, then one fused adjoint + epilogue + forward iteration per
+// launch), U = Σ_r Z_r w_r all-reduced between launches, and at checks the rank's check totals and
+// Z_r β⁺ all-reduced before a decision kernel (admm.cu step_decide).  Z_r is read once per iteration.
+int bound_sharded_fused(Ctx* c, int B, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
+                        const double* warm_in, const double* parent_lb, double* lb, double* primal, double* warm_out,
+                        int32_t* iters, uint8_t* flags, cudaStream_t st) {
+  const int64_t pr = c->p;
+  // fixings (GLOBAL column indices) → this rank's local columns
+  std::vector<int64_t> off(B + 1, 0), loff(B + 1, 0);
+  std::vector<int32_t> idx, lidx;
+  std::vector<uint8_t> val, lval;
+  if (fix_off) {
+    L0L2_CUDA(c, cudaMemcpyAsync(off.data(), fix_off, sizeof(int64_t) * (B + 1), cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    idx.resize(off[B]);
+    val.resize(off[B]);
+    if (off[B] > 0) {
+      L0L2_CUDA(c, cudaMemcpyAsync(idx.data(), fix_idx, sizeof(int32_t) * off[B], cudaMemcpyDeviceToHost, st));
+      L0L2_CUDA(c, cudaMemcpyAsync(val.data(), fix_val, off[B], cudaMemcpyDeviceToHost, st));
+      L0L2_CUDA(c, cudaStreamSynchronize(st));
+    }
+    for (int k = 0; k < B; k++) {
+      for (int64_t q = off[k]; q < off[k + 1]; q++) {
+        const int64_t j = (int64_t)idx[q] - c->col0;
+        if (idx[q] < 0 || idx[q] >= c->p_total) return set_err(c, L0L2_EINVAL, "fixing index out of range");
+        if (j < 0 || j >= pr) continue;
+        lidx.push_back((int32_t)j);
+        lval.push_back(val[q]);
+      }
+      loff[k + 1] = (int64_t)lidx.size();
+    }
+  }
+  int64_t* d_off = (int64_t*)c->scratch_n(2, sizeof(int64_t) * (B + 1) + sizeof(double) * kBC * 4 + 64);
+  int32_t* d_idx = (int32_t*)c->scratch_n(3, sizeof(int32_t) * std::max<size_t>(1, lidx.size()));
+  uint8_t* d_val = (uint8_t*)c->scratch_n(4, std::max<size_t>(1, lval.size()));
+  double** wptr = (double**)c->scratch_n(5, sizeof(double*) * 2 * kBC);
+  if (!d_off || !d_idx || !d_val || !wptr) return set_err(c, L0L2_ENOMEM, "sharded scratch");
+  double* tot = (double*)((char*)d_off + ((sizeof(int64_t) * (B + 1) + 63) / 64) * 64);
+  L0L2_CUDA(c, cudaMemcpyAsync(d_off, loff.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
+  if (!lidx.empty()) {
+    L0L2_CUDA(c, cudaMemcpyAsync(d_idx, lidx.data(), sizeof(int32_t) * lidx.size(), cudaMemcpyHostToDevice, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(d_val, lval.data(), lval.size(), cudaMemcpyHostToDevice, st));
+  }
+  bool notconv = false;
+  int rc = L0L2_OK;
+  for (int g0 = 0; g0 < B; g0 += kBC) {
+    const int nb = std::min(kBC, B - g0);
+    const double* hin[kBC] = {};
+    double* hout[kBC] = {};
+    for (int k = 0; k < nb; k++) {
+      hin[k] = warm_in ? warm_in + (int64_t)(g0 + k) * 2 * pr : nullptr;
+      hout[k] = warm_out ? warm_out + (int64_t)(g0 + k) * 2 * pr : nullptr;
+    }
+    L0L2_CUDA(c, cudaMemcpyAsync(wptr, hin, sizeof(hin), cudaMemcpyHostToDevice, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(wptr + kBC, hout, sizeof(hout), cudaMemcpyHostToDevice, st));
+    if ((rc = pack_group(c, nb, fix_off ? d_off + g0 : nullptr, d_idx, d_val, (const double* const*)wptr, st))) return rc;
+    BoundArgs a{nb, parent_lb ? parent_lb + g0 : nullptr, lb + g0, primal + g0, iters + g0, flags + g0};
+    if (!warm_in) a.cold_mask = (1u << nb) - 1u;
+    const int64_t ucount = (int64_t)kBC * c->ld;
+    if ((rc = admm_step(c, a, 0, 0, tot, st)) || (rc = shard_allreduce(c, c->U, ucount, st))) return rc;
+    if (warm_in && ((rc = admm_step(c, a, 1, 0, tot, st)) || (rc = shard_allreduce(c, c->U, ucount, st)))) return rc;
+    int hfl[2 * kBC];
+    for (int it = 1; it <= c->max_iters; it++) {
+      const int chk = (it % c->check_every == 0) || it == c->max_iters;
+      if ((rc = admm_step(c, a, 2, chk, tot, st)) || (rc = shard_allreduce(c, c->U, ucount, st))) return rc;
+      if (!chk) continue;
+      if ((rc = shard_allreduce(c, tot, kBC * 4, st)) || (rc = shard_allreduce(c, c->Ub, ucount, st)) ||
+          (rc = admm_step_decide(c, a, it, tot, st)))
+        return rc;
+      L0L2_CUDA(c, cudaMemcpyAsync(hfl, c->node_i, sizeof(hfl), cudaMemcpyDeviceToHost, st));
+      L0L2_CUDA(c, cudaStreamSynchronize(st));
+      bool any = false;
+      for (int k = 0; k < nb; k++) any |= (hfl[2 * k] & 64) != 0;   // F_ACTIVE (admm.cu)
+      if (!any) break;
+    }
+    if ((rc = admm_step_outputs(c, a, st))) return rc;
+    if (warm_out && (rc = unpack_warm(c, nb, wptr + kBC, st))) return rc;
+    uint8_t hf[kBC];
+    L0L2_CUDA(c, cudaMemcpyAsync(hf, flags + g0, nb, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    for (int k = 0; k < nb; k++) notconv |= (hf[k] & L0L2_FLAG_MAXITER) != 0;
+  }
+  return notconv ? L0L2_WNOTCONV : L0L2_OK;
+}
+
 // Column-sharded bound of B nodes (see the file header).  Device pointers, ordered on `stream`.
 int bound_sharded(Ctx* c, int B, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
                   const double* warm_in, const double* parent_lb, double* lb, double* primal, double* warm_out,
                   int32_t* iters, uint8_t* flags, cudaStream_t st) {
+  const char* eg = getenv("L0L2_SHARD_GEMM");   // test hook: the unfused GEMM loop below
+  if (c->shard_fused && !(eg && atoi(eg) != 0))
+    return bound_sharded_fused(c, B, fix_off, fix_idx, fix_val, warm_in, parent_lb, lb, primal, warm_out, iters,
+                               flags, st);
   const int64_t pr = c->p, n = c->n, ld = c->ld;
   // work space: code, β, v, w, s (B × pr), u / Xβ (B × ld), terms (B × 4) + Xβ (B × ld) exchange block
   const size_t need = (size_t)B * pr * (1 + 8 * 4) + sizeof(double) * ((size_t)B * ld * 2 + (size_t)B * 4) + 64 * B + 4096;

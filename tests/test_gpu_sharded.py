@@ -38,8 +38,9 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, mode, q):
+def _worker(rank, world, port, mode, impl, q):
     import torch.distributed as dist
+    os.environ["L0L2_SHARD_GEMM"] = "1" if impl == "gemm" else "0"
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -69,12 +70,12 @@ def _worker(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-def _run(mode, world=2):
+def _run(mode, impl, world=2):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, impl, q)) for r in range(world)]
     for p in procs:
         p.start()
     out = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
@@ -85,11 +86,14 @@ def _run(mode, world=2):
     return out
 
 
+@pytest.mark.parametrize("impl", ["fused", "gemm"])
 @pytest.mark.parametrize("mode", ["fixed", "converged"])
-def test_two_rank_column_sharded_bounds_equal_the_oracle(mode):
+def test_two_rank_column_sharded_bounds_equal_the_oracle(mode, impl):
+    """impl "fused": the persistent ADMM kernel in step mode on each rank's shard (one launch per
+    iteration, U all-reduced between launches); "gemm": the unfused reference loop."""
     inst, lam0, lam2, M = _instance()
     P = O.Problem(inst.X, inst.y, lam0, lam2, M)
-    out = _run(mode)
+    out = _run(mode, impl)
     fx = _fixings(inst)
     kw = dict(node_tol=-1.0, max_iters=37) if mode == "fixed" else dict(node_tol=1e-7, max_iters=20000)
     # every rank returns the same bounds, iterations and flags

@@ -2,6 +2,7 @@
 C4's columns (W = 1, 2, 4, 8 → p/W columns; no exchange), fixed iterations, B nodes.  The W-rank time
 per iteration ≈ this + one all-reduce of n·B doubles (and of n·B + 4B at checks)."""
 import json
+import os
 import sys
 import time
 
@@ -30,4 +31,4 @@ for W in (1, 2, 4, 8):
         dt = time.perf_counter() - t
         rows.append(dict(W=W, p_r=pr, B=B, ms_per_iteration=dt / iters * 1e3))
     sp.close()
-print(json.dumps(rows))
+print(json.dumps(dict(impl="gemm" if os.environ.get("L0L2_SHARD_GEMM") == "1" else "fused", rows=rows)))
