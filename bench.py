@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--micro-iters", type=int, default=100)
     ap.add_argument("--seeds", type=int, default=10, help="C2 seeds for the certified-solve median / IQR")
     ap.add_argument("--c5-time-limit", type=float, default=8.0, help="per-λ0 time limit of the C5 sweep (0: skip)")
+    ap.add_argument("--paper-corr", type=float, default=0.1)
+    ap.add_argument("--paper-time-limit", type=float, default=20.0,
+                    help="time limit of the n=3000, p=30000 (P:878) solve through the wide-n path (0: skip)")
     ap.add_argument("--oracle-bnb", default="C2", help="config of the measured oracle BnB legs ('' to skip)")
     ap.add_argument("--verbose", action="store_true")
     return ap.parse_args()
@@ -583,6 +586,42 @@ def main():
     except Exception as e:   # context sections never cost the headline line
         section_errors['c5sweep'] = repr(e)
 
+    # the paper's own n = 3000, p = 30000 workload (SNR 10/3, k = 10, λ2 / λ0 / M by the recipe,
+    # DESIGN.md §5) — beyond the fused kernel's n ≤ 1056, so it runs the wide-n ADMM path: a fixed-iteration
+    # microbenchmark (B 1 / 16) and a time-limited solve with the MP incumbent + early prune
+    paper = None
+    try:
+        if world == 1 and args.paper_time_limit > 0:
+            import synth
+            instp = synth.make_instance(3000, 30000, 10, args.paper_corr, 10.0 / 3.0, args.seed)
+            instp.lambda2 = synth.tune_lambda2(instp)
+            instp.lambda0 = synth.lambda0_rule(instp, instp.lambda2)
+            instp.M = synth.bigM_rule(instp, instp.lambda2)
+            rhop = float(np.mean(np.einsum("ij,ij->j", instp.X, instp.X))) * args.rho_mult
+            paper = {"workload": "synthetic n=3000 p=30000 k*=10 corr=%g SNR=10/3 seed %d (P:878 baseline)"
+                                 % (args.paper_corr, args.seed),
+                     "lambda0": instp.lambda0, "lambda2": instp.lambda2, "M": instp.M, "rho": rhop}
+            mb = bound_microbench(instp, rhop, local, 50, Bs=(1, 16))
+            paper["bound_microbench"] = mb
+            prp = Problem(np.asfortranarray(instp.X), instp.y, instp.lambda0, instp.lambda2, instp.M, rho=rhop,
+                          node_tol=1e-4, max_iters=10000, device=local)
+            paper["admm_path"] = prp.info()["admm_path"]
+            torch.cuda.synchronize(dev)
+            t = time.perf_counter()
+            rp = prp.l0l2_solve(gap_tol=1e-2, batch=args.batch, init_mp=True, early_prune=True,
+                                time_limit_s=args.paper_time_limit)
+            dtp = time.perf_counter() - t
+            stp = rp["stats"]
+            paper["solve"] = {"gap_tol": 1e-2, "node_tol": 1e-4, "init_mp": True, "early_prune": True,
+                              "time_limit_s": args.paper_time_limit, "time_s": dtp, "certified": stp["status"] <= 1,
+                              "gap": rp["gap"], "nodes": stp["nodes"], "nodes_per_s": stp["nodes"] / dtp,
+                              "node_iters_per_s": stp["node_iters"] / dtp, "objective": rp["obj"],
+                              "support": [int(j) for j in rp["support"]],
+                              "planted_support": [int(j) for j in instp.support_true]}
+            prp.close()
+    except Exception as e:   # context sections never cost the headline line
+        section_errors['paper_n3000'] = repr(e)
+
     # time-to-certified-optimality at the full C4 size: the recipe's λ0* leaves a tree that does not
     # close in minutes; λ0 = 2·λ0* (one of the paper's λ0-path multipliers) certifies a 1% gap
     c4cert = None
@@ -665,6 +704,8 @@ def main():
                     elif "time_s_median" in r and r["time_s_median"] is not None:   # the C2 seeds block
                         ttc["C2 seeds 0-%d median gap %g%s" % (args.seeds - 1, blk["gap_tol"], " +MP+early prune"
                                                                 if r["init_mp"] else "")] = r["time_s_median"]
+            if paper is not None and paper.get("solve", {}).get("certified"):
+                ttc["n=3000 p=30000 (P:878) gap 0.01 +MP+early prune"] = paper["solve"]["time_s"]
         except Exception as e:
             line.setdefault("section_errors", {})["time_to_certified_optimality"] = repr(e)
         line["time_to_certified_optimality"] = {"unit": "s", "runs": ttc,
@@ -672,6 +713,8 @@ def main():
                                                         "instance (key = config, lambda0, gap_tol, options)"}
         if c5sweep is not None:
             line["c5_lambda0_sweep"] = c5sweep
+        if paper is not None:
+            line["paper_n3000_wide_path"] = paper
         if mp is not None:
             line["matching_pursuit"] = mp
         if cpu is not None:

@@ -66,8 +66,10 @@ void l0l2_default_opts(l0l2_opts* o);
  * typo corrected, R1).  X and y are copied (host or device per opts->x_on_device)
  * and never aliased afterwards.  For p ≤ 2n (and p ≤ 1056) the direct regime is used: D =
  * (XᵀX + ρI)⁻¹ = (I − ZᵀZ)/ρ is precomputed (p×p) and the bound kernel streams D (R17).
- * Errors: L0L2_EINVAL (see above, and n > 1056 outside the direct regime: the ADMM kernel's 3-stage
- * tile ring of Z must fit one CTA's shared memory), L0L2_ENOMEM, L0L2_ECUDA.
+ * For n > 1056 outside the direct regime (the fused kernel's tile ring of Z no longer fits one CTA's
+ * shared memory) the node bounds run on the wide-n path (l0l2_admm_path = 2): same arithmetic and
+ * outputs, Z streamed twice per iteration.
+ * Errors: L0L2_EINVAL (see above), L0L2_ENOMEM, L0L2_ECUDA.
  * On error *out is NULL.
  */
 int l0l2_create(const double* X, const double* y, int64_t n, int64_t p,
@@ -285,6 +287,15 @@ int l0l2_kernel_stats(l0l2_ctx* ctx, l0l2_kstats* out, int32_t reset);
  * also the peak), and kernel launches so far. */
 int l0l2_info(const l0l2_ctx* ctx, int64_t* n, int64_t* p, double* rho, int64_t* device_bytes,
               int64_t* kernel_launches);
+
+/* Which ADMM implementation the context's node bounds run on:
+ *   0 = the fused persistent kernel, Z-form (Z = L⁻¹X streamed once per iteration);
+ *   1 = the fused persistent kernel, direct regime b = D w (p ≤ 2n, R17);
+ *   2 = the wide-n path (n beyond the fused kernel's on-chip budget, n > 1056): a column-tiled
+ *       adjoint + epilogue kernel and a split-K forward GEMM per iteration, same node state and
+ *       arithmetic (Z read twice per iteration).
+ * Negative on a null context. */
+int l0l2_admm_path(const l0l2_ctx* ctx);
 
 const char* l0l2_last_error(const l0l2_ctx* ctx);
 void l0l2_destroy(l0l2_ctx* ctx);

@@ -109,6 +109,8 @@ def load_library():
     lib.l0l2_bound_sharded.restype = C.c_int
     lib.l0l2_info.argtypes = [P] + [P] * 5
     lib.l0l2_info.restype = C.c_int
+    lib.l0l2_admm_path.argtypes = [P]
+    lib.l0l2_admm_path.restype = C.c_int
     lib.l0l2_last_error.argtypes = [P]
     lib.l0l2_last_error.restype = C.c_char_p
     lib.l0l2_destroy.argtypes = [P]
@@ -268,7 +270,9 @@ class Problem:
         rho = C.c_double()
         _check(self._lib.l0l2_info(self._ctx, C.byref(n), C.byref(p), C.byref(rho), C.byref(dev), C.byref(launches)),
                self._ctx)
-        return dict(n=n.value, p=p.value, rho=rho.value, device_bytes=dev.value, kernel_launches=launches.value)
+        path = self._lib.l0l2_admm_path(self._ctx)
+        return dict(n=n.value, p=p.value, rho=rho.value, device_bytes=dev.value, kernel_launches=launches.value,
+                    admm_path={0: "fused-zform", 1: "fused-direct", 2: "wide-n"}.get(path, path))
 
     def l0l2_kernel_stats(self, reset=False):
         ks = _KStats()

@@ -1338,6 +1338,522 @@ __global__ void step_outputs(KP k) {
   k.out_flags[nd] = (uint8_t)(k.nodei[nd * 2] & (L0L2_FLAG_CONVERGED | L0L2_FLAG_MAXITER));
 }
 
+// ---------------------------------------------------------------- wide-n path
+// The fused kernel keeps u (n×8) and its forward accumulators (n×8) in registers and a 3-stage ring
+// of n×8 Z tiles in shared memory, which caps n at 1056.  Beyond that (the paper's n = 3000 and
+// 11 962 workloads) the SAME iteration runs on the same node state (stt, node_f/node_i,
+// bchk) as a host-stepped sequence:
+//   wide_sweep   S_J = Z_Jᵀu for 64 columns per CTA (DMMA, K = n split over 8 warps, u read from L2,
+//                fixed-order cross-warp tree), then the fused kernel's elementwise epilogue (b, β⁺, v⁺,
+//                w⁺, check terms) — one read of Z;
+//   gemm_f64     u⁺ = Z w⁺ (n × 16, K = p, deterministic split-K) — the second read of Z;
+//   at checks    Xβ⁺ (GEMM) for ‖Xβ‖², then wide_decide: dual, primal, running
+//                max (R7), stop (R8), early prune (R16) — the fused kernel's decision arithmetic.
+// Z is streamed twice per iteration instead of once; every sum has a fixed order.
+constexpr int WT = 8;                 // 8-column tiles per CTA of wide_sweep
+constexpr int WTH = 256;              // 8 warps
+constexpr int WEL = WT * kPt * kBC;   // (column, node) elements per CTA
+
+// w = c + ρβ − v of the active nodes (0 for the others), [p8][kBC]; keeps the nodes' starting
+// iteration counts (a resumed node continues its count)
+__global__ void __launch_bounds__(WTH) wide_w0(KP k, double* W, int* it0) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.x == 0 && threadIdx.x < kBC) it0[threadIdx.x] = k.nodei[threadIdx.x * 2 + 1];
+  if (e >= k.p8 * kBC) return;
+  const int64_t j = e / kBC;
+  const int nd = (int)(e % kBC);
+  double w = 0.0;
+  if (k.nodei[nd * 2] & F_ACTIVE) {
+    const int64_t o = st_beta(j, nd);
+    w = k.stt[st_c(j)] + k.rho * k.stt[o] - k.stt[o + STB];
+  }
+  W[e] = w;
+}
+
+template <bool REFRESH>
+__global__ void __launch_bounds__(WTH) wide_sweep(KP k, int check, double* W, double* Bb, double* wsum) {
+  __shared__ double red[4][WEL];        // cross-warp partials of S (32 KB)
+  __shared__ double csum[WTH / kBC][kBC][4];
+  __shared__ int fl[kBC];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < kBC) fl[tid] = k.nodei[tid * 2];
+  __syncthreads();
+  const int t0 = blockIdx.x * WT;
+  const int nt = min(WT, k.ntiles - t0);
+  const int cA = lane >> 2, kA = lane & 3;
+  // ---- adjoint S_J = Z_Jᵀ u for the CTA's tiles: A = Z_Jᵀ (8 cols × 4 rows), B = u (4 rows × 8 nodes);
+  // warp w takes the k-steps ≡ w (mod 8)
+  double acc[WT][2][2];
+#pragma unroll
+  for (int t = 0; t < WT; t++) acc[t][0][0] = acc[t][0][1] = acc[t][1][0] = acc[t][1][1] = 0.0;
+  {
+    const bool a0 = (fl[cA] & F_ACTIVE) != 0, a1 = (fl[8 + cA] & F_ACTIVE) != 0;
+    const double* U0 = k.U + (int64_t)cA * k.ld + kA;
+    const double* U1 = k.U + (int64_t)(8 + cA) * k.ld + kA;
+    const double* Zb = k.Z + ((int64_t)t0 * kPt + cA) * k.ld + kA;
+    const int kt = (int)((k.n + 3) / 4);   // rows past n: Z and u are zero there (ld ≥ round8(n))
+#pragma unroll 2
+    for (int q = warp; q < kt; q += WTH / 32) {
+      const double u0 = a0 ? __ldcg(U0 + 4 * q) : 0.0;
+      const double u1 = a1 ? __ldcg(U1 + 4 * q) : 0.0;
+      double a[WT];
+#pragma unroll
+      for (int t = 0; t < WT; t++) a[t] = t < nt ? __ldcs(Zb + (int64_t)t * kPt * k.ld + 4 * q) : 0.0;
+#pragma unroll
+      for (int t = 0; t < WT; t++) {
+        dmma(acc[t][0], a[t], u0);
+        dmma(acc[t][1], a[t], u1);
+      }
+    }
+  }
+  // fixed-order tree over the 8 warps: (w, w+4), then (w, w+2), then (w, w+1)
+  auto put = [&](double* dst) {
+#pragma unroll
+    for (int t = 0; t < WT; t++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        dst[t * 128 + cA * kBC + 8 * h + 2 * kA] = acc[t][h][0];
+        dst[t * 128 + cA * kBC + 8 * h + 2 * kA + 1] = acc[t][h][1];
+      }
+  };
+  for (int half = 4; half >= 1; half >>= 1) {
+    if (warp >= half && warp < 2 * half) put(red[warp - half]);
+    __syncthreads();
+    if (warp < half) {
+      const double* src = red[warp];
+#pragma unroll
+      for (int t = 0; t < WT; t++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          acc[t][h][0] += src[t * 128 + cA * kBC + 8 * h + 2 * kA];
+          acc[t][h][1] += src[t * 128 + cA * kBC + 8 * h + 2 * kA + 1];
+        }
+    }
+    __syncthreads();
+  }
+  if (warp == 0) put(red[0]);
+  __syncthreads();
+  // ---- epilogue (the fused sweep's arithmetic): thread tid owns node tid % 16 of 4 columns
+  const int node = tid & (kBC - 1);
+  const bool active = (fl[node] & F_ACTIVE) != 0, cold = (fl[node] & F_COLD) != 0;
+  double sT1 = 0.0, sT2 = 0.0, sT3 = 0.0, sT4 = 0.0;
+#pragma unroll
+  for (int i = 0; i < WEL / WTH; i++) {
+    const int e = tid + WTH * i, t = e >> 7, el = e & 127, jj = el >> 4;
+    if (t >= nt) continue;
+    const int64_t tile = t0 + t, col = tile * kPt + jj;
+    double* q = k.stt + tile * STQ;
+    const double q_beta = q[el], q_v = q[STB + el], q_c = q[2 * STB + jj];
+    const uint8_t q_code = reinterpret_cast<const uint8_t*>(q + 2 * STB + 8)[el];
+    const double sv = red[0][e];
+    const double w = q_c + k.rho * q_beta - q_v;
+    double wn = 0.0, bo = 0.0;
+    if (active) {
+      const double b = (w - sv) * k.inv_rho;                          // b = D w, D = (I − ZᵀZ)/ρ (R1)
+      const double bn = REFRESH ? q_beta : prox(k, b + q_v * k.inv_rho, q_code);
+      const double vn = (REFRESH && cold) ? q_v : q_v + k.rho * (b - bn);   // cold: (0, 0), no refresh (R6)
+      if (check) {
+        sT1 = fma(b, sv, sT1);                                        // bᵀ(XᵀX b)
+        sT2 += nu_f(k, fabs(q_c - sv), q_code);                      // Σ ν(|Xᵀr̂|)
+        sT3 = fma(q_c, bn, sT3);                                      // cᵀβ
+        sT4 += psi_f(k, bn, q_code);                                  // Σ ψ(β)
+        k.bchk[col * kBC + node] = b;
+      }
+      q[el] = bn;
+      q[STB + el] = vn;
+      wn = q_c + k.rho * bn - vn;
+      bo = bn;
+    }
+    W[col * kBC + node] = wn;
+    if (check) Bb[col * kBC + node] = bo;
+  }
+  if (!check) return;
+  csum[tid >> 4][node][0] = sT1;
+  csum[tid >> 4][node][1] = sT2;
+  csum[tid >> 4][node][2] = sT3;
+  csum[tid >> 4][node][3] = sT4;
+  __syncthreads();
+  if (tid < kBC * 4) {
+    const int nd = tid >> 2, term = tid & 3;
+    double a = 0.0;
+    for (int g = 0; g < WTH / kBC; g++) a += csum[g][nd][term];
+    wsum[((int64_t)blockIdx.x * kBC + nd) * 4 + term] = a;
+  }
+}
+
+// Forward product for the wide-n path: dst = A W (n × 16, K = p) for A = Z (u⁺ = Z w⁺) or X (Xβ⁺ at
+// checks).  CTA (x, y) owns rows [512x, 512x + 512) and the column chunk y; each warp 64 rows (8 DMMA
+// row tiles × 2 node halves in registers), k-steps of 4 columns streamed from HBM once; the chunk
+// partials are summed in chunk order by wide_reduce (deterministic).
+constexpr int WFR = 512;
+__global__ void __launch_bounds__(WTH) wide_forward(const double* __restrict__ A, int64_t ld, int64_t n, int64_t p8,
+                                                    const double* __restrict__ W, int64_t cpc, double* part) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, cA = lane >> 2, kA = lane & 3;
+  const int64_t r0 = (int64_t)blockIdx.x * WFR + warp * 64;
+  const int64_t c0 = (int64_t)blockIdx.y * cpc, c1 = min(p8, c0 + cpc);
+  double acc[8][2][2];
+  bool rv[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    acc[i][0][0] = acc[i][0][1] = acc[i][1][0] = acc[i][1][1] = 0.0;
+    rv[i] = r0 + 8 * i + cA < n;
+  }
+  const double* Ab = A + (c0 + kA) * ld + r0 + cA;
+  const double* Wb = W + (c0 + kA) * kBC + cA;
+#pragma unroll 2
+  for (int64_t c = c0; c < c1; c += 4) {
+    const int64_t o = (c - c0);
+    const double b0 = __ldg(Wb + o * kBC), b1 = __ldg(Wb + o * kBC + 8);
+    double a[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) a[i] = rv[i] ? __ldcs(Ab + o * ld + 8 * i) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      dmma(acc[i][0], a[i], b0);
+      dmma(acc[i][1], a[i], b1);
+    }
+  }
+  double* pb = part + (int64_t)blockIdx.y * kBC * ld;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    if (!rv[i]) continue;
+    const int64_t row = r0 + 8 * i + cA;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      pb[(int64_t)(8 * h + 2 * kA) * ld + row] = acc[i][h][0];
+      pb[(int64_t)(8 * h + 2 * kA + 1) * ld + row] = acc[i][h][1];
+    }
+  }
+}
+// ---- pipelined variants (default): each warp streams its share of Z through its own cp.async ring in
+// shared memory (no registers held by loads in flight, no CTA barrier inside the K loop), one CTA per SM.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr(dst)), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+constexpr int WPS = 4;                       // ring stages per warp
+constexpr int WGT = 4;                       // tiles per group of the pipelined sweep (32 columns)
+constexpr int WGC = WGT * kPt;               // 32 columns
+constexpr int WGE = WGC * kBC;               // (column, node) elements per group
+constexpr int WSR = 16;                      // rows per stage (4 k-steps)
+constexpr int WLDS = WSR + 2;                // smem doubles per column of a stage (padded)
+constexpr int WSTG = WGC * WLDS;             // doubles per stage (4.5 KB)
+constexpr size_t WSWEEP_SMEM = sizeof(double) * ((size_t)(WTH / 32) * WPS * WSTG + 4 * WGE);   // 160 KB
+
+// Persistent over groups of 32 columns (4 tiles); warp w owns every 8th 16-row stage of the group
+// (4 k-steps each), so u is read once per group and Z once per sweep.  A warp issues
+// the first stages of its next group before the cross-warp tree and the epilogue of the current one,
+// so HBM keeps streaming through them.  Epilogue and check sums: wide_sweep's arithmetic and order.
+template <bool REFRESH>
+__global__ void __launch_bounds__(WTH, 1) wide_sweep_p(KP k, int check, double* W, double* Bb, double* wsum) {
+  extern __shared__ __align__(16) double wsm[];
+  __shared__ double csum[WTH / kBC][kBC][4];
+  __shared__ int fl[kBC];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cA = lane >> 2, kA = lane & 3;
+  if (tid < kBC) fl[tid] = k.nodei[tid * 2];
+  __syncthreads();
+  const bool a0 = (fl[cA] & F_ACTIVE) != 0, a1 = (fl[8 + cA] & F_ACTIVE) != 0;
+  int any0 = 0, any1 = 0;
+  for (int nd = 0; nd < 8; nd++) { any0 |= fl[nd] & F_ACTIVE; any1 |= fl[8 + nd] & F_ACTIVE; }
+  const int ngroups = (k.ntiles + WGT - 1) / WGT;
+  const int US = (int)((k.n8 + WSR - 1) / WSR);                     // 16-row stages per column
+  // warp w takes the stages w, w + 8, w + 16, ... of every column (at any moment the CTA's warps read
+  // adjacent 16-row blocks: 1 KB runs per column rather than 128-B pieces of 8 distant slabs)
+  constexpr int NWP = WTH / 32;
+  const int nsw = US > warp ? (US - warp + NWP - 1) / NWP : 0;
+  double* ring = wsm + (size_t)warp * WPS * WSTG;
+  double* red = wsm + (size_t)(WTH / 32) * WPS * WSTG;             // [4][WGE]
+  const double* Ur0 = k.U + (int64_t)cA * k.ld + kA;
+  const double* Ur1 = k.U + (int64_t)(8 + cA) * k.ld + kA;
+  // stage m (in this warp's global sequence: group g_m = blockIdx.x + (m / nsw)·gridDim.x, stage m % nsw)
+  // → ring slot m % WPS.  Rows past n8 and columns past p8 are zero-filled.
+  auto issue = [&](int m) {
+    const int gi = nsw > 0 ? m / nsw : 0;
+    const int g = blockIdx.x + gi * gridDim.x;
+    if (nsw > 0 && g < ngroups) {
+      const int t0 = g * WGT, ncol = min(WGT, k.ntiles - t0) * kPt;
+      const double* Zg = k.Z + (int64_t)t0 * kPt * k.ld;
+      double* dst = ring + (m % WPS) * WSTG;
+      const int64_t row0 = (int64_t)(warp + NWP * (m % nsw)) * WSR;
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const int c = lane + 32 * i, col = c >> 3, part = c & 7;
+        const bool ok = col < ncol && row0 + 2 * part < k.n8;
+        cp_async16(dst + col * WLDS + 2 * part, ok ? Zg + (int64_t)col * k.ld + row0 + 2 * part : k.Z, ok ? 16 : 0);
+      }
+    }
+    cp_commit();
+  };
+  int m = 0;   // this warp's next stage to consume
+#pragma unroll
+  for (int q = 0; q < WPS - 1; q++) issue(q);
+  // u rows of a stage (a0 / a1: the lane's nodes cA, 8 + cA), loaded one stage ahead (L2 latency off the
+  // DMMA path)
+  double ua[4], ub[4];
+  auto load_u = [&](int sI, double* xa, double* xb) {
+    const int64_t row0 = (int64_t)(warp + NWP * sI) * WSR;
+#pragma unroll
+    for (int ks = 0; ks < 4; ks++) {
+      xa[ks] = (a0 && nsw > 0) ? __ldcg(Ur0 + row0 + 4 * ks) : 0.0;
+      xb[ks] = (a1 && nsw > 0) ? __ldcg(Ur1 + row0 + 4 * ks) : 0.0;
+    }
+  };
+  load_u(0, ua, ub);
+  for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const int t0 = g * WGT;
+    const int nt = min(WGT, k.ntiles - t0);
+    double acc[WGT][2][2];
+#pragma unroll
+    for (int t = 0; t < WGT; t++) acc[t][0][0] = acc[t][0][1] = acc[t][1][0] = acc[t][1][1] = 0.0;
+    for (int sI = 0; sI < nsw; sI++, m++) {
+      issue(m + WPS - 1);
+      double na[4], nb[4];
+      load_u(sI + 1 < nsw ? sI + 1 : 0, na, nb);   // the next stage's rows (the next group restarts at 0)
+      cp_wait<WPS - 1>();
+      __syncwarp();
+      const double* b = ring + (m % WPS) * WSTG + cA * WLDS + kA;
+#pragma unroll
+      for (int ks = 0; ks < 4; ks++) {
+        double x[WGT];
+#pragma unroll
+        for (int t = 0; t < WGT; t++) x[t] = b[t * kPt * WLDS + 4 * ks];
+        if (any0) {
+#pragma unroll
+          for (int t = 0; t < WGT; t++) dmma(acc[t][0], x[t], ua[ks]);
+        }
+        if (any1) {
+#pragma unroll
+          for (int t = 0; t < WGT; t++) dmma(acc[t][1], x[t], ub[ks]);
+        }
+      }
+      __syncwarp();   // the slot is refilled by a later issue
+#pragma unroll
+      for (int ks = 0; ks < 4; ks++) { ua[ks] = na[ks]; ub[ks] = nb[ks]; }
+    }
+    // the next group's first stages are already in flight (issue runs WPS − 1 stages ahead)
+    auto put = [&](double* dst) {
+#pragma unroll
+      for (int t = 0; t < WGT; t++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          dst[t * 128 + cA * kBC + 8 * h + 2 * kA] = acc[t][h][0];
+          dst[t * 128 + cA * kBC + 8 * h + 2 * kA + 1] = acc[t][h][1];
+        }
+    };
+    for (int half = 4; half >= 1; half >>= 1) {
+      if (warp >= half && warp < 2 * half) put(red + (warp - half) * WGE);
+      __syncthreads();
+      if (warp < half) {
+        const double* src = red + warp * WGE;
+#pragma unroll
+        for (int t = 0; t < WGT; t++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            acc[t][h][0] += src[t * 128 + cA * kBC + 8 * h + 2 * kA];
+            acc[t][h][1] += src[t * 128 + cA * kBC + 8 * h + 2 * kA + 1];
+          }
+      }
+      __syncthreads();
+    }
+    if (warp == 0) put(red);
+    __syncthreads();
+    const int node = tid & (kBC - 1);
+    const bool active = (fl[node] & F_ACTIVE) != 0, cold = (fl[node] & F_COLD) != 0;
+    double sT1 = 0.0, sT2 = 0.0, sT3 = 0.0, sT4 = 0.0;
+#pragma unroll
+    for (int i = 0; i < WGE / WTH; i++) {
+      const int e = tid + WTH * i, t = e >> 7, el = e & 127, jj = el >> 4;
+      if (t >= nt) continue;
+      const int64_t tile = t0 + t, col = tile * kPt + jj;
+      double* q = k.stt + tile * STQ;
+      const double q_beta = q[el], q_v = q[STB + el], q_c = q[2 * STB + jj];
+      const uint8_t q_code = reinterpret_cast<const uint8_t*>(q + 2 * STB + 8)[el];
+      const double sv = red[e];
+      const double w = q_c + k.rho * q_beta - q_v;
+      double wn = 0.0, bo = 0.0;
+      if (active) {
+        const double b = (w - sv) * k.inv_rho;                                // b = D w, D = (I − ZᵀZ)/ρ (R1)
+        const double bn = REFRESH ? q_beta : prox(k, b + q_v * k.inv_rho, q_code);
+        const double vn = (REFRESH && cold) ? q_v : q_v + k.rho * (b - bn);   // cold: (0, 0), no refresh (R6)
+        if (check) {
+          sT1 = fma(b, sv, sT1);                                              // bᵀ(XᵀX b)
+          sT2 += nu_f(k, fabs(q_c - sv), q_code);                            // Σ ν(|Xᵀr̂|)
+          sT3 = fma(q_c, bn, sT3);                                            // cᵀβ
+          sT4 += psi_f(k, bn, q_code);                                        // Σ ψ(β)
+          k.bchk[col * kBC + node] = b;
+        }
+        q[el] = bn;
+        q[STB + el] = vn;
+        wn = q_c + k.rho * bn - vn;
+        bo = bn;
+      }
+      W[col * kBC + node] = wn;
+      if (check) Bb[col * kBC + node] = bo;
+    }
+    if (check) {
+      csum[tid >> 4][node][0] = sT1;
+      csum[tid >> 4][node][1] = sT2;
+      csum[tid >> 4][node][2] = sT3;
+      csum[tid >> 4][node][3] = sT4;
+      __syncthreads();
+      if (tid < kBC * 4) {
+        const int nd = tid >> 2, term = tid & 3;
+        double a = 0.0;
+        for (int q = 0; q < WTH / kBC; q++) a += csum[q][nd][term];
+        wsum[((int64_t)g * kBC + nd) * 4 + term] = a;
+      }
+    }
+    __syncthreads();   // red and csum are reused by the next group
+  }
+  cp_wait<0>();
+}
+
+// dst = A W with per-warp cp.async rings: CTA (x, y) owns rows [256x, 256x + 256) and column chunk y;
+// warp w streams rows 32w..32w+31 of the chunk in stages of 16 columns (4 k-steps, 4 KB) and keeps
+// its 32 × 16 output block in registers (4 row tiles × 2 node halves).
+constexpr int WFPR = 256;                    // rows per CTA
+constexpr int WFPC = 16;                     // columns per stage
+constexpr int WFLD = 36;                     // smem doubles per column of a stage (32 rows + pad)
+constexpr int WFSTG = WFPC * WFLD;
+constexpr size_t WFWD_SMEM = sizeof(double) * (size_t)(WTH / 32) * WPS * WFSTG;   // 144 KB
+__global__ void __launch_bounds__(WTH, 1) wide_forward_p(const double* __restrict__ A, int64_t ld, int64_t n8,
+                                                         int64_t p8, const double* __restrict__ W, int64_t cpc,
+                                                         double* part) {
+  extern __shared__ __align__(16) double wsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, cA = lane >> 2, kA = lane & 3;
+  const int64_t r0 = (int64_t)blockIdx.x * WFPR + warp * 32;
+  const int64_t c0 = (int64_t)blockIdx.y * cpc, c1 = min(p8, c0 + cpc);
+  const int nst = (int)((c1 - c0 + WFPC - 1) / WFPC);
+  double* ring = wsm + (size_t)warp * WPS * WFSTG;
+  auto issue = [&](int m) {
+    if (m < nst) {
+      double* dst = ring + (m % WPS) * WFSTG;
+      const int64_t cb = c0 + (int64_t)m * WFPC;
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const int c = lane + 32 * i, col = c >> 4, part = c & 15;
+        const int64_t row = r0 + 2 * part;
+        const bool ok = cb + col < c1 && row < n8;
+        cp_async16(dst + col * WFLD + 2 * part, ok ? A + (cb + col) * ld + row : A, ok ? 16 : 0);
+      }
+    }
+    cp_commit();
+  };
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; i++) acc[i][0][0] = acc[i][0][1] = acc[i][1][0] = acc[i][1][1] = 0.0;
+#pragma unroll
+  for (int m = 0; m < WPS - 1; m++) issue(m);
+  // the stage's w rows (B fragments), loaded one stage ahead
+  auto load_w = [&](int m, double* x0, double* x1) {
+    const int64_t cb = c0 + (int64_t)m * WFPC;
+#pragma unroll
+    for (int ks = 0; ks < 4; ks++) {
+      const bool ok = m < nst && cb + 4 * ks + kA < c1;
+      x0[ks] = ok ? __ldg(W + (cb + 4 * ks + kA) * kBC + cA) : 0.0;
+      x1[ks] = ok ? __ldg(W + (cb + 4 * ks + kA) * kBC + 8 + cA) : 0.0;
+    }
+  };
+  double b0[4], b1[4];
+  load_w(0, b0, b1);
+  for (int m = 0; m < nst; m++) {
+    issue(m + WPS - 1);
+    double n0[4], n1[4];
+    load_w(m + 1, n0, n1);
+    cp_wait<WPS - 1>();
+    __syncwarp();
+    const double* b = ring + (m % WPS) * WFSTG + kA * WFLD + cA;
+#pragma unroll
+    for (int ks = 0; ks < 4; ks++) {
+      double x[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) x[i] = b[4 * ks * WFLD + 8 * i];
+#pragma unroll
+      for (int i = 0; i < 4; i++) dmma(acc[i][0], x[i], b0[ks]);
+#pragma unroll
+      for (int i = 0; i < 4; i++) dmma(acc[i][1], x[i], b1[ks]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int ks = 0; ks < 4; ks++) { b0[ks] = n0[ks]; b1[ks] = n1[ks]; }
+  }
+  cp_wait<0>();
+  double* pb = part + (int64_t)blockIdx.y * kBC * ld;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const int64_t row = r0 + 8 * i + cA;
+    if (row >= n8) continue;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      pb[(int64_t)(8 * h + 2 * kA) * ld + row] = acc[i][h][0];
+      pb[(int64_t)(8 * h + 2 * kA + 1) * ld + row] = acc[i][h][1];
+    }
+  }
+}
+
+__global__ void wide_reduce(int64_t n, int64_t ld, int nchunk, const double* __restrict__ part, double* dst) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * kBC) return;
+  const int64_t row = e % n, nd = e / n;
+  double a = 0.0;
+  for (int y = 0; y < nchunk; y++) a += part[((int64_t)y * kBC + nd) * ld + row];
+  dst[nd * ld + row] = a;
+}
+
+// per node: the check totals (CTA partials in fixed order), ‖Xβ⁺‖², and the fused kernel's decision
+__global__ void __launch_bounds__(WTH) wide_decide(KP k, int it, int nblk, const double* __restrict__ wsum,
+                                                   const double* __restrict__ XB, const int* __restrict__ it0) {
+  const int nd = blockIdx.x, tid = threadIdx.x;
+  int fl = k.nodei[nd * 2];
+  if (!(fl & F_ACTIVE)) return;
+  __shared__ double red[WTH / 32][5];
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int q = tid; q < nblk; q += WTH)
+    for (int t = 0; t < 4; t++) v[t] += wsum[((int64_t)q * kBC + nd) * 4 + t];
+  for (int64_t i = tid; i < k.xn; i += WTH) {
+    const double x = XB[(int64_t)nd * k.xld + i];
+    v[4] = fma(x, x, v[4]);
+  }
+  for (int t = 0; t < 5; t++)
+    for (int o = 16; o > 0; o >>= 1) v[t] += __shfl_xor_sync(0xffffffffu, v[t], o);
+  if ((tid & 31) == 0)
+    for (int t = 0; t < 5; t++) red[tid >> 5][t] = v[t];
+  __syncthreads();
+  if (tid != 0) return;
+  double T[5];
+  for (int t = 0; t < 5; t++) {
+    T[t] = 0.0;
+    for (int w = 0; w < WTH / 32; w++) T[t] += red[w][t];
+  }
+  const double dual = 0.5 * k.yy - 0.5 * T[0] - T[1];
+  const double primal = 0.5 * k.yy - T[2] + 0.5 * T[4] + T[3];
+  const double lbb = fmax(k.nodef[nd * 4 + 0], dual);   // running max of checked duals (R7)
+  const double pub = k.prune_ub_dev ? *k.prune_ub_dev : k.prune_ub;
+  if ((primal - lbb) / fmax(1.0, fabs(primal)) <= k.node_tol) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_CONVERGED;
+  else if (lbb >= pub) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_PRUNED;   // early prune (R16)
+  else if (it0[nd] + it >= k.max_iters) fl = (fl & ~F_ACTIVE) | L0L2_FLAG_MAXITER;
+  k.nodef[nd * 4 + 0] = lbb;
+  k.nodef[nd * 4 + 1] = primal;
+  k.nodef[nd * 4 + 3] = dual;
+  k.nodei[nd * 2 + 0] = fl;
+  k.nodei[nd * 2 + 1] = it0[nd] + it;
+}
+
+__global__ void wide_outputs(KP k) {
+  const int nd = threadIdx.x;
+  if (nd >= k.nb || !((k.act_mask >> nd) & 1u)) return;
+  const double lbb = k.nodef[nd * 4 + 0];
+  k.out_lb[nd] = fmax(lbb, k.nodef[nd * 4 + 2]);
+  k.out_primal[nd] = k.nodef[nd * 4 + 1];
+  k.out_iters[nd] = k.nodei[nd * 2 + 1];
+  k.out_flags[nd] = (uint8_t)(k.nodei[nd * 2] & (L0L2_FLAG_CONVERGED | L0L2_FLAG_MAXITER | L0L2_FLAG_PRUNED));
+  if (k.out_lbbest) k.out_lbbest[nd] = lbb;
+}
+
 using AdmmKernel = void (*)(KP);
 template <bool DIR>
 AdmmKernel admm_kernel_t(int cls) {
@@ -1378,14 +1894,65 @@ size_t admm_smem_bytes(int64_t ld) {
          (NST + 4) * sizeof(uint64_t) + 3 * kBC * sizeof(int) + (2 * NST + 12) * sizeof(int) + NST * sizeof(unsigned) + 64;
 }
 
+int admm_alloc_wide(Ctx* c) {
+  const int64_t p8 = round8(c->p), ld = c->ld;
+  const int64_t nblk = (p8 / kPt + WGT - 1) / WGT;   // check-sum blocks (groups of the sweep, ≤ 4 tiles)
+  c->wide = 1;
+  c->admm_cls = -1;
+  c->grid = 0;
+  c->stt = (double*)dalloc(c, sizeof(double) * (p8 / kPt) * STQ);
+  if (c->stt) L0L2_CUDA(c, cudaMemset(c->stt, 0, sizeof(double) * (p8 / kPt) * STQ));
+  c->bchk = (double*)dalloc(c, sizeof(double) * p8 * kBC);
+  c->U = (double*)dalloc(c, sizeof(double) * kBC * ld);
+  c->wW = (double*)dalloc(c, sizeof(double) * p8 * kBC);
+  c->wB = (double*)dalloc(c, sizeof(double) * p8 * kBC);
+  c->wXB = (double*)dalloc(c, sizeof(double) * kBC * ld);
+  c->wsum = (double*)dalloc(c, sizeof(double) * nblk * kBC * 4);
+  c->wit0 = (int*)dalloc(c, sizeof(int) * kBC);
+  c->wide_v1 = 0;
+  if (const char* e = getenv("L0L2_WIDE_V1")) c->wide_v1 = atoi(e) != 0;   // tuning hook: register-prefetch kernels
+  if (c->wide_v1) {
+    // forward grid: row blocks × column chunks (≥ 64 columns each, a multiple of 4), ≈ 2 CTAs per SM
+    c->wrb = (int)((c->n + WFR - 1) / WFR);
+    c->wcc = (int)std::max<int64_t>(1, std::min<int64_t>(p8 / 64, (2 * c->sms + c->wrb - 1) / c->wrb));
+    c->wcpc = ((p8 + c->wcc - 1) / c->wcc + 3) / 4 * 4;
+  } else {
+    // one CTA per SM: row blocks × column chunks ≤ #SMs (chunks ≥ 64 columns, a multiple of a stage)
+    c->wrb = (int)((round8(c->n) + WFPR - 1) / WFPR);
+    c->wcc = (int)std::max<int64_t>(1, std::min<int64_t>(p8 / 64, c->sms / c->wrb));
+    c->wcpc = ((p8 + c->wcc - 1) / c->wcc + WFPC - 1) / WFPC * WFPC;
+    L0L2_CUDA(c, cudaFuncSetAttribute(wide_sweep_p<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSWEEP_SMEM));
+    L0L2_CUDA(c, cudaFuncSetAttribute(wide_sweep_p<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSWEEP_SMEM));
+    L0L2_CUDA(c, cudaFuncSetAttribute(wide_forward_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WFWD_SMEM));
+  }
+  c->wcc = (int)((p8 + c->wcpc - 1) / c->wcpc);
+  c->wpart = (double*)dalloc(c, sizeof(double) * c->wcc * kBC * ld);
+  c->node_f = (double*)dalloc(c, sizeof(double) * kBC * 4);
+  c->node_i = (int*)dalloc(c, sizeof(int) * kBC * 2);
+  c->badflag = (int*)dalloc(c, sizeof(int));
+  if (!c->stt || !c->bchk || !c->U || !c->wW || !c->wB || !c->wXB || !c->wsum || !c->wit0 || !c->wpart || !c->node_f ||
+      !c->node_i || !c->badflag)
+    return set_err(c, L0L2_ENOMEM, "admm work space (wide-n path)");
+  // rows n..ld of u stay 0 (the adjoint reads whole 4-row k-steps); padding columns of β, v stay 0
+  L0L2_CUDA(c, cudaMemset(c->U, 0, sizeof(double) * kBC * ld));
+  L0L2_CUDA(c, cudaMemset(c->bchk, 0, sizeof(double) * p8 * kBC));
+  return L0L2_OK;
+}
+
 int admm_alloc(Ctx* c) {
   // the streamed operand: Z (n×p, ld) or, in the direct regime, D (p×p, ldD)
   const int64_t p8 = round8(c->p), ld = c->direct ? c->ldD : c->ld;
   const int64_t kn = c->direct ? c->p : c->n;
   c->admm_cls = admm_class(round8(kn));
-  if (c->admm_cls < 0)
-    return set_err(c, L0L2_EINVAL, "n = %lld > %d not supported by the fused ADMM kernel", (long long)c->n,
-                   std::min(4 * NMW * CLS_KS[NCLS - 1], 8 * NMW * CLS_MT[NCLS - 1]));
+  // the fused kernel's on-chip budget: n8 within its register classes and the 3-stage ring of n×8
+  // tiles in shared memory (n ≤ 1056); beyond it (Z-form only) the wide-n path
+  bool fits = c->admm_cls >= 0 && admm_smem_bytes(ld) + 1024 <= 227 * 1024;
+  if (const char* e = getenv("L0L2_WIDE"))   // test hook: force the wide-n path
+    if (atoi(e) != 0 && !c->direct) fits = false;
+  if (!fits) {
+    if (c->direct) return set_err(c, L0L2_EINVAL, "direct regime: p = %lld too large", (long long)c->p);
+    return admm_alloc_wide(c);
+  }
   const int ntiles = (int)(p8 / kPt);
   // an even grid: CTA pairs (2P, 2P+1) serve the two node halves; a sub-range may be empty.  At
   // least 2 tiles per CTA: for small p an iteration is latency-bound, and fewer CTAs cut the grid
@@ -1479,11 +2046,19 @@ bool admm_paired(const Ctx* c) {
   return true;
 }
 
+int run_admm_wide(Ctx* c, const BoundArgs& a, cudaStream_t st);
+
 int run_admm(Ctx* c, const BoundArgs& a, cudaStream_t st) {
   if (!c->ev[0]) {
     for (auto& e : c->ev) L0L2_CUDA(c, cudaEventCreate(&e));
   }
   L0L2_CUDA(c, cudaEventRecord(c->ev[0], st));
+  if (c->wide) {
+    const int rc = run_admm_wide(c, a, st);
+    if (rc) return rc;
+    L0L2_CUDA(c, cudaEventRecord(c->ev[1], st));
+    return L0L2_OK;
+  }
   const bool split = a.nb > 8 && !admm_paired(c);
   const unsigned all = (1u << a.nb) - 1u;
   const unsigned masks[2] = {split ? (all & 0xFFu) : all, all & 0xFF00u};
@@ -1537,6 +2112,69 @@ int admm_step_decide(Ctx* c, const BoundArgs& a, int it, const double* tot, cuda
 int admm_step_outputs(Ctx* c, const BoundArgs& a, cudaStream_t st) {
   KP k = make_kp(c, a, (1u << a.nb) - 1u);
   step_outputs<<<1, 32, 0, st>>>(k);
+  L0L2_LAUNCHED(c);
+  return L0L2_OK;
+}
+
+// The wide-n path (see wide_sweep): one group of ≤ 16 nodes, all its iterations, host-stepped; the
+// host reads the 16 node flags after each check (the loop's only synchronisation).
+int run_admm_wide(Ctx* c, const BoundArgs& a, cudaStream_t st) {
+  const unsigned mask = (1u << a.nb) - 1u;
+  init_nodes<<<1, 32, 0, st>>>(a.nb, mask, a.cold_mask, a.parent_lb, a.lbbest_in, a.it0_in, a.warm_ptrs, c->node_f,
+                               c->node_i);
+  L0L2_LAUNCHED(c);
+  const KP k = make_kp(c, a, mask);
+  const int nblk = c->wide_v1 ? (k.ntiles + WT - 1) / WT : (k.ntiles + WGT - 1) / WGT;   // check-sum blocks
+  const unsigned sgrid = c->wide_v1 ? (unsigned)nblk : (unsigned)std::min(nblk, c->sms);
+  auto sweep = [&](bool refresh, int chk) {
+    if (c->wide_v1) {
+      if (refresh) wide_sweep<true><<<sgrid, WTH, 0, st>>>(k, chk, c->wW, c->wB, c->wsum);
+      else wide_sweep<false><<<sgrid, WTH, 0, st>>>(k, chk, c->wW, c->wB, c->wsum);
+    } else {
+      if (refresh) wide_sweep_p<true><<<sgrid, WTH, WSWEEP_SMEM, st>>>(k, chk, c->wW, c->wB, c->wsum);
+      else wide_sweep_p<false><<<sgrid, WTH, WSWEEP_SMEM, st>>>(k, chk, c->wW, c->wB, c->wsum);
+    }
+    L0L2_LAUNCHED(c);
+    return L0L2_OK;
+  };
+  auto forward_of = [&](const double* A, const double* W, double* dst) {   // dst = A W (n × 16, K = p)
+    if (c->wide_v1)
+      wide_forward<<<dim3((unsigned)c->wrb, (unsigned)c->wcc), WTH, 0, st>>>(A, c->ld, c->n, k.p8, W, c->wcpc, c->wpart);
+    else
+      wide_forward_p<<<dim3((unsigned)c->wrb, (unsigned)c->wcc), WTH, WFWD_SMEM, st>>>(A, c->ld, k.n8, k.p8, W, c->wcpc,
+                                                                                        c->wpart);
+    L0L2_LAUNCHED(c);
+    wide_reduce<<<(unsigned)((c->n * kBC + 255) / 256), 256, 0, st>>>(c->n, c->ld, c->wcc, c->wpart, dst);
+    L0L2_LAUNCHED(c);
+    return L0L2_OK;
+  };
+  auto forward = [&](const double* W, double* dst) { return forward_of(c->Z, W, dst); };
+  // u0 = Z(c + ρβ0 − v0), then the warm-start refresh (R6) and its u
+  wide_w0<<<(unsigned)((k.p8 * kBC + WTH - 1) / WTH), WTH, 0, st>>>(k, c->wW, c->wit0);
+  L0L2_LAUNCHED(c);
+  int rc = forward(c->wW, c->U);
+  if (rc) return rc;
+  if ((rc = sweep(true, 0)) || (rc = forward(c->wW, c->U))) return rc;
+  int hn[2 * kBC];
+  L0L2_CUDA(c, cudaMemcpyAsync(hn, c->node_i, sizeof(hn), cudaMemcpyDeviceToHost, st));
+  L0L2_CUDA(c, cudaStreamSynchronize(st));
+  int it0[kBC];
+  for (int nd = 0; nd < kBC; nd++) it0[nd] = hn[2 * nd + 1];
+  for (int it = 1; it <= c->max_iters; it++) {
+    bool chk = (it % c->check_every == 0) || (it == c->max_iters);
+    for (int nd = 0; nd < kBC; nd++) chk |= (hn[2 * nd] & F_ACTIVE) && it0[nd] + it == c->max_iters;
+    if ((rc = sweep(false, chk ? 1 : 0)) || (rc = forward(c->wW, c->U))) return rc;
+    if (!chk) continue;
+    if ((rc = forward_of(c->X, c->wB, c->wXB))) return rc;
+    wide_decide<<<kBC, WTH, 0, st>>>(k, it, nblk, c->wsum, c->wXB, c->wit0);
+    L0L2_LAUNCHED(c);
+    L0L2_CUDA(c, cudaMemcpyAsync(hn, c->node_i, sizeof(hn), cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    bool any = false;
+    for (int nd = 0; nd < kBC; nd++) any |= (hn[2 * nd] & F_ACTIVE) != 0;
+    if (!any) break;
+  }
+  wide_outputs<<<1, 32, 0, st>>>(k);
   L0L2_LAUNCHED(c);
   return L0L2_OK;
 }

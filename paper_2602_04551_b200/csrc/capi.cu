@@ -213,7 +213,7 @@ int create_impl(const double* X, const double* y, int64_t n, int64_t p, double l
     ok = rc == L0L2_OK;
   }
   if (ok && sh) {    // a sharded context runs the same kernel in step mode on its shard when n fits
-    c->shard_fused = admm_alloc(c) == L0L2_OK ? 1 : 0;
+    c->shard_fused = (admm_alloc(c) == L0L2_OK && !c->wide) ? 1 : 0;
     c->err.clear();
   }
   cudaStreamSynchronize(st);
@@ -277,6 +277,12 @@ int l0l2_info(const l0l2_ctx* ctx, int64_t* n, int64_t* p, double* rho, int64_t*
   }
   if (launches) *launches = c->launches;
   return L0L2_OK;
+}
+
+int l0l2_admm_path(const l0l2_ctx* ctx) {
+  if (!ctx) return L0L2_EINVAL;
+  const Ctx* c = &ctx->impl;
+  return c->wide ? 2 : (c->direct ? 1 : 0);
 }
 
 int l0l2_bound_batch(l0l2_ctx* ctx, int32_t B, const int64_t* fix_off, const int32_t* fix_idx,

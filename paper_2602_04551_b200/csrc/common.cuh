@@ -70,6 +70,16 @@ struct Ctx {
   size_t ub_scratch_bytes = 0;
   int grid = 0;
   int admm_cls = -1;                                        // n class of the ADMM kernel (admm.cu)
+  // wide-n path (admm.cu): n beyond the fused kernel's on-chip budget; host-stepped kernels + GEMMs
+  int wide = 0;
+  double *wW = nullptr, *wB = nullptr;                      // w⁺ and β⁺ at checks, [p8][kBC]
+  double *wXB = nullptr;                                    // Xβ⁺ at checks, [kBC][ld]
+  double *wsum = nullptr;                                   // per-CTA check sums [nblk][kBC][4]
+  int *wit0 = nullptr;                                      // iterations of the nodes before the launch
+  double *wpart = nullptr;                                  // forward partials per column chunk [wcc][kBC][ld]
+  int wrb = 0, wcc = 0;                                     // forward grid: row blocks × column chunks
+  int wide_v1 = 0;                                          // register-prefetch kernels instead of cp.async rings
+  int64_t wcpc = 0;                                         // columns per chunk
   // scratch for batch I/O in solve (device)
   std::vector<void*> owned;
   int64_t bytes = 0;

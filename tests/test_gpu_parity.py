@@ -393,14 +393,6 @@ def test_solve_with_mp_incumbent(seed):
     prob.close()
 
 
-def test_n_beyond_the_tile_ring_is_rejected():
-    """n whose 3-stage Z tile ring does not fit one CTA's shared memory: a clean L0L2_EINVAL."""
-    inst = synth.make_instance(1064, 2200, 3, 0.3, 4.0, 1)   # p > 2n: Z-form (the direct regime streams D)
-    with pytest.raises(L0L2Error) as e:
-        Problem(inst.X, inst.y, 1.0, 0.5, 2.0)
-    assert e.value.code == -1 and "shared memory" in str(e.value)
-
-
 @pytest.mark.parametrize("n", [1008, 1056])
 def test_largest_n_classes(n):
     """The two largest n classes of the ADMM kernel (n8 = 1008, and 1056 = the largest n whose tile

@@ -16,7 +16,12 @@ HBM = 6540.8
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
 Bs = [int(b) for b in (sys.argv[2] if len(sys.argv) > 2 else "1,8,16").split(",")]
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 100
-inst = synth.config_instance(cfg, seed=0)
+if cfg == "P3000":   # the paper's n = 3000, p = 30000 workload, wide-n ADMM path
+    inst = synth.make_instance(3000, 30000, 10, 0.1, 10.0 / 3.0, 0)
+    lam2 = synth.tune_lambda2(inst)
+    inst.lambda2, inst.lambda0, inst.M = lam2, synth.lambda0_rule(inst, lam2), synth.bigM_rule(inst, lam2)
+else:
+    inst = synth.config_instance(cfg, seed=0)
 rho = 3.0 * float(np.mean(np.einsum("ij,ij->j", inst.X, inst.X)))
 pr = Problem(inst.X, inst.y, inst.lambda0, inst.lambda2, inst.M, rho=rho, node_tol=-1.0, max_iters=iters)
 fx = [((), ())] + synth.random_fixings(inst.p, max(Bs) - 1, seed=11, depth_lo=5, depth_hi=10, prefer=inst.support_true)
