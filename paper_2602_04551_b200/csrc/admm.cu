@@ -1557,8 +1557,6 @@ __global__ void __launch_bounds__(WTH, 1) wide_sweep_p(KP k, int check, double* 
   if (tid < kBC) fl[tid] = k.nodei[tid * 2];
   __syncthreads();
   const bool a0 = (fl[cA] & F_ACTIVE) != 0, a1 = (fl[8 + cA] & F_ACTIVE) != 0;
-  int any0 = 0, any1 = 0;
-  for (int nd = 0; nd < 8; nd++) { any0 |= fl[nd] & F_ACTIVE; any1 |= fl[8 + nd] & F_ACTIVE; }
   const int ngroups = (k.ntiles + WGT - 1) / WGT;
   const int US = (int)((k.n8 + WSR - 1) / WSR);                     // 16-row stages per column
   // warp w takes the stages w, w + 8, w + 16, ... of every column (at any moment the CTA's warps read
@@ -1602,37 +1600,64 @@ __global__ void __launch_bounds__(WTH, 1) wide_sweep_p(KP k, int check, double* 
       xb[ks] = (a1 && nsw > 0) ? __ldcg(Ur1 + row0 + 4 * ks) : 0.0;
     }
   };
+  // u rows two stages ahead, rotating three register sets (L2 latency under full HBM load exceeds one
+  // stage of DMMAs)
+  double va[4], vb[4], wa[4], wb[4];
   load_u(0, ua, ub);
+  load_u(nsw > 1 ? 1 : 0, va, vb);
   for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
     const int t0 = g * WGT;
     const int nt = min(WGT, k.ntiles - t0);
     double acc[WGT][2][2];
 #pragma unroll
     for (int t = 0; t < WGT; t++) acc[t][0][0] = acc[t][0][1] = acc[t][1][0] = acc[t][1][1] = 0.0;
-    for (int sI = 0; sI < nsw; sI++, m++) {
+    // one stage: refill the ring WPS − 1 ahead, load the next stage's u rows into (na, nb), compute
+    // with (xa, xb); the loop below alternates the two u register sets (no copies on the load path)
+    auto step = [&](int sI, const double* xa, const double* xb, double* na, double* nb) {
       issue(m + WPS - 1);
-      double na[4], nb[4];
-      load_u(sI + 1 < nsw ? sI + 1 : 0, na, nb);   // the next stage's rows (the next group restarts at 0)
+      load_u((sI + 2) % nsw, na, nb);   // two stages ahead (the next group restarts at 0)
       cp_wait<WPS - 1>();
       __syncwarp();
-      const double* b = ring + (m % WPS) * WSTG + cA * WLDS + kA;
+      const double* bp = ring + (m % WPS) * WSTG + cA * WLDS + kA;
 #pragma unroll
       for (int ks = 0; ks < 4; ks++) {
         double x[WGT];
 #pragma unroll
-        for (int t = 0; t < WGT; t++) x[t] = b[t * kPt * WLDS + 4 * ks];
-        if (any0) {
+        for (int t = 0; t < WGT; t++) x[t] = bp[t * kPt * WLDS + 4 * ks];
 #pragma unroll
-          for (int t = 0; t < WGT; t++) dmma(acc[t][0], x[t], ua[ks]);
-        }
-        if (any1) {
+        for (int t = 0; t < WGT; t++) dmma(acc[t][0], x[t], xa[ks]);
 #pragma unroll
-          for (int t = 0; t < WGT; t++) dmma(acc[t][1], x[t], ub[ks]);
-        }
+        for (int t = 0; t < WGT; t++) dmma(acc[t][1], x[t], xb[ks]);
       }
       __syncwarp();   // the slot is refilled by a later issue
+      m++;
+    };
+    // stage sI computes with set sI % 3 and loads stage sI + 2 into set (sI + 2) % 3; at the end of a group
+    // the sets are rotated so that set 0 holds stage 0 of the next group (once per group, off the hot loop)
+    int sI = 0;
+    for (; sI + 3 <= nsw; sI += 3) {
+      step(sI, ua, ub, wa, wb);
+      step(sI + 1, va, vb, ua, ub);
+      step(sI + 2, wa, wb, va, vb);
+    }
+    if (sI < nsw) step(sI, ua, ub, wa, wb), sI++;
+    if (sI < nsw) step(sI, va, vb, ua, ub), sI++;
+    // now (sI % 3) names the set holding stage 0 of the next group, the following set stage 1
+    if (nsw % 3 == 1) {
 #pragma unroll
-      for (int ks = 0; ks < 4; ks++) { ua[ks] = na[ks]; ub[ks] = nb[ks]; }
+      for (int q = 0; q < 4; q++) {
+        const double t0a = va[q], t0b = vb[q];
+        va[q] = wa[q]; vb[q] = wb[q];   // stage 1 (loaded into w)
+        ua[q] = t0a; ub[q] = t0b;       // stage 0 (loaded into v)
+      }
+    } else if (nsw % 3 == 2) {
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const double t0a = wa[q], t0b = wb[q];
+        wa[q] = ua[q]; wb[q] = ub[q];
+        va[q] = wa[q]; vb[q] = wb[q];   // stage 1 (loaded into u)
+        ua[q] = t0a; ub[q] = t0b;       // stage 0 (loaded into w)
+      }
     }
     // the next group's first stages are already in flight (issue runs WPS − 1 stages ahead)
     auto put = [&](double* dst) {
@@ -1758,28 +1783,31 @@ __global__ void __launch_bounds__(WTH, 1) wide_forward_p(const double* __restric
       x1[ks] = ok ? __ldg(W + (cb + 4 * ks + kA) * kBC + 8 + cA) : 0.0;
     }
   };
-  double b0[4], b1[4];
+  double b0[4], b1[4], n0[4], n1[4];
   load_w(0, b0, b1);
-  for (int m = 0; m < nst; m++) {
+  int m = 0;
+  auto step = [&](const double* x0w, const double* x1w, double* y0w, double* y1w) {
     issue(m + WPS - 1);
-    double n0[4], n1[4];
-    load_w(m + 1, n0, n1);
+    load_w(m + 1, y0w, y1w);
     cp_wait<WPS - 1>();
     __syncwarp();
-    const double* b = ring + (m % WPS) * WFSTG + kA * WFLD + cA;
+    const double* bp = ring + (m % WPS) * WFSTG + kA * WFLD + cA;
 #pragma unroll
     for (int ks = 0; ks < 4; ks++) {
       double x[4];
 #pragma unroll
-      for (int i = 0; i < 4; i++) x[i] = b[4 * ks * WFLD + 8 * i];
+      for (int i = 0; i < 4; i++) x[i] = bp[4 * ks * WFLD + 8 * i];
 #pragma unroll
-      for (int i = 0; i < 4; i++) dmma(acc[i][0], x[i], b0[ks]);
+      for (int i = 0; i < 4; i++) dmma(acc[i][0], x[i], x0w[ks]);
 #pragma unroll
-      for (int i = 0; i < 4; i++) dmma(acc[i][1], x[i], b1[ks]);
+      for (int i = 0; i < 4; i++) dmma(acc[i][1], x[i], x1w[ks]);
     }
     __syncwarp();
-#pragma unroll
-    for (int ks = 0; ks < 4; ks++) { b0[ks] = n0[ks]; b1[ks] = n1[ks]; }
+    m++;
+  };
+  while (m < nst) {
+    step(b0, b1, n0, n1);
+    if (m < nst) step(n0, n1, b0, b1);
   }
   cp_wait<0>();
   double* pb = part + (int64_t)blockIdx.y * kBC * ld;
