@@ -323,7 +323,7 @@ def run_reference(args):
             vals.append(cb["value"])
     v = float(np.mean(vals))
     line = {"metric": "BnB nodes/sec", "value": v, "unit": "nodes/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "%s seed %d: %s" % (args.config, args.seed, CONFIG_DESC[args.config]),
                        "gap_tol": args.gap_tol, "node_tol": args.node_tol, "node_limit": args.node_limit,
@@ -403,7 +403,9 @@ def main():
     t = time.perf_counter()
     prob = make_problem(Xh, inst.y)
     t_create = time.perf_counter() - t
-    solve_kw = dict(gap_tol=args.gap_tol, batch=args.batch, node_limit=args.node_limit,
+    # weak scaling: the frontier is partitioned over the ranks (north star), so each GPU solves a fixed
+    # share of the tree prefix — node_limit is per GPU, the solve stops after node_limit × W nodes in total
+    solve_kw = dict(gap_tol=args.gap_tol, batch=args.batch, node_limit=args.node_limit * world,
                     verbose=args.verbose and rank == 0)
     for _ in range(args.warmup):
         res = prob.l0l2_solve(**solve_kw)
@@ -660,10 +662,11 @@ def main():
         st = last["stats"]
         line = {"metric": "BnB nodes/sec", "value": value, "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": "%s seed %d: %s" % (args.config, args.seed, CONFIG_DESC[args.config]),
                            "lambda0": inst.lambda0, "lambda2": inst.lambda2, "M": inst.M, "rho": rho,
-                           "gap_tol": args.gap_tol, "node_tol": args.node_tol, "node_limit": args.node_limit,
+                           "gap_tol": args.gap_tol, "node_tol": args.node_tol,
+                           "node_limit_per_gpu": args.node_limit, "node_limit": args.node_limit * world,
                            "batch": args.batch,
                            "parallelism": ("frontier partitioned over %d GPU(s)" % world) if not shared else
                            ("DRY RUN: %d ranks share %d GPU(s), exchange over the host transport (gloo)"

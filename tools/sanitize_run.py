@@ -6,6 +6,8 @@ usage: compute-sanitizer --tool <tool> python tools/sanitize_run.py <case>
   c2      C2-shaped (n=p=1000, direct regime) 16-node batch, fixed 12 iterations
   zform   p > 2n Z-form (n=200, p=2000): 17-node batch with convergence (compaction), the dense
           primal fallback (L0L2_NZCAP=0) and a short solve with early prune + MP
+  wide    the wide-n path: forced (L0L2_WIDE=1) on a ragged Z-form instance (17-node batch with warm
+          starts, a short solve with MP + early prune) and natural at n = 1064 (16 nodes)
 """
 import os
 import sys
@@ -64,6 +66,21 @@ def main(case):
         sp = ShardedProblem(inst.X[:, :700], inst.y, 0, 700, 1.0, 2.0, 2.0, node_tol=1e-6, max_iters=300)
         sp.l0l2_bound_sharded([((), ()), ((1,), (3,))])
         sp.close()
+    elif case == "wide":
+        os.environ["L0L2_WIDE"] = "1"
+        inst = synth.make_instance(61, 203, 4, 0.3, 4.0, 9)
+        lam2 = 0.5
+        lam0, M = synth.lambda0_rule(inst, lam2), synth.bigM_rule(inst, lam2)
+        pr = Problem(inst.X, inst.y, lam0, lam2, M, node_tol=1e-7, max_iters=300)
+        out = pr.l0l2_bound_batch(fixings(inst, 17, 5), want_zhat=True, want_dual_r=True)
+        pr.l0l2_bound_batch(fixings(inst, 3, 6), warm_in=out["warm_out"][:3].contiguous())
+        pr.l0l2_solve(gap_tol=1e-3, batch=16, node_limit=60, init_mp=True, early_prune=True)
+        pr.close()
+        del os.environ["L0L2_WIDE"]
+        inst = synth.make_instance(1064, 2200, 5, 0.3, 4.0, 31)
+        pr = Problem(np.asfortranarray(inst.X), inst.y, 1.0, 0.5, 2.0, node_tol=-1.0, max_iters=12)
+        pr.l0l2_bound_batch(fixings(inst, 16, 7))
+        pr.close()
     print("sanitize case %s done" % case)
 
 
