@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--micro-iters", type=int, default=100)
     ap.add_argument("--seeds", type=int, default=10, help="C2 seeds for the certified-solve median / IQR")
     ap.add_argument("--c5-time-limit", type=float, default=8.0, help="per-λ0 time limit of the C5 sweep (0: skip)")
+    ap.add_argument("--coop-rampup", action="store_true",
+                    help="W > 1: column-sharded cooperative ramp-up (l0l2_solve_opts.coop_rampup)")
     ap.add_argument("--paper-corr", type=float, default=0.1)
     ap.add_argument("--paper-time-limit", type=float, default=20.0,
                     help="time limit of the n=3000, p=30000 (P:878) solve through the wide-n path (0: skip)")
@@ -406,6 +408,7 @@ def main():
     # weak scaling: the frontier is partitioned over the ranks (north star), so each GPU solves a fixed
     # share of the tree prefix — node_limit is per GPU, the solve stops after node_limit × W nodes in total
     solve_kw = dict(gap_tol=args.gap_tol, batch=args.batch, node_limit=args.node_limit * world,
+                    coop_rampup=args.coop_rampup,
                     verbose=args.verbose and rank == 0)
     for _ in range(args.warmup):
         res = prob.l0l2_solve(**solve_kw)

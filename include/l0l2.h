@@ -165,6 +165,12 @@ typedef struct {
                                they stopped in the next launch, next to fresh nodes.  Bounds and the
                                certificate are unchanged; the tree order (node ids) differs from the
                                synchronous rounds.  Single rank only.  0 (default): synchronous      */
+  int32_t coop_rampup;      /* multi-GPU: 1 → until the frontier is
+                               partitioned (every rank holds the same tree), the ranks solve each node
+                               of a round TOGETHER through the column-sharded bound (rank r: its column
+                               block of Z, one all-reduce of u per iteration) instead of each solving
+                               all of them; the blocks of the final (β, v) are all-gathered into full warm
+                               states.  Needs ≥ 8 columns per rank.  0 (default): redundant ramp-up   */
 } l0l2_solve_opts;
 
 void l0l2_default_solve_opts(l0l2_solve_opts* o);
@@ -182,6 +188,7 @@ typedef struct {
   int32_t support_size;
   int64_t nodes_moved;      /* open nodes moved between ranks by frontier rebalancing (Σ over ranks) */
   int64_t suspensions;      /* continuous batching: node suspensions (each node resumed later)       */
+  int64_t coop_rounds;      /* rounds solved cooperatively (column-sharded ramp-up, coop_rampup)      */
 } l0l2_stats;
 
 /*

@@ -30,7 +30,7 @@ class _SolveOpts(C.Structure):
     _fields_ = [("gap_tol", C.c_double), ("time_limit_s", C.c_double), ("node_limit", C.c_int64),
                 ("batch", C.c_int32), ("rebalance_every", C.c_int32), ("warm_bytes_cap", C.c_int64),
                 ("verbose", C.c_int32), ("record", C.c_int32), ("init_mp", C.c_int32),
-                ("early_prune", C.c_int32), ("continuous", C.c_int32)]
+                ("early_prune", C.c_int32), ("continuous", C.c_int32), ("coop_rampup", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -39,7 +39,7 @@ class _Stats(C.Structure):
                 ("t_total", C.c_double), ("t_bound", C.c_double), ("t_upper", C.c_double), ("t_tree", C.c_double),
                 ("t_comm", C.c_double), ("lb", C.c_double), ("ub", C.c_double), ("gap", C.c_double),
                 ("status", C.c_int32), ("support_size", C.c_int32), ("nodes_moved", C.c_int64),
-                ("suspensions", C.c_int64)]
+                ("suspensions", C.c_int64), ("coop_rounds", C.c_int64)]
 
 
 class _KStats(C.Structure):
@@ -382,7 +382,8 @@ class Problem:
         self.l0l2_comm_init(dist.get_world_size(), dist.get_rank(), obj[0])
 
     def l0l2_solve(self, gap_tol=1e-2, batch=16, time_limit_s=0.0, node_limit=0, rebalance_every=8,
-                   warm_bytes_cap=0, verbose=False, record=False, init_mp=False, early_prune=False, continuous=0):
+                   warm_bytes_cap=0, verbose=False, record=False, init_mp=False, early_prune=False, continuous=0,
+                   coop_rampup=False):
         so = _SolveOpts()
         self._lib.l0l2_default_solve_opts(C.byref(so))
         so.gap_tol, so.batch, so.time_limit_s = float(gap_tol), int(batch), float(time_limit_s)
@@ -392,6 +393,7 @@ class Problem:
         so.init_mp = int(bool(init_mp))
         so.early_prune = int(bool(early_prune))
         so.continuous = int(continuous)
+        so.coop_rampup = int(bool(coop_rampup))
         beta = np.zeros(self.p, dtype=np.float64)
         obj, gap = C.c_double(), C.c_double()
         st = _Stats()

@@ -204,7 +204,8 @@ __device__ __forceinline__ double nu_f(const KP& k, double x, uint8_t code) {   
 #define L0L2_NST 3
 #endif
 constexpr int NST = L0L2_NST;  // Z tile stages in the TMA ring (3 × 64.75 KB at n = 1000)
-constexpr int PFD_DEFAULT = 1; // additional tiles prefetched into L2 beyond the smem ring (k.pfd)
+constexpr int PFD_DEFAULT = 0; // tiles prefetched into L2 beyond the smem ring (k.pfd); 0 measured best on the C4 step
+                               // (92.6 vs 89.2 nodes/s, profiles/sweeps_r02/) and at C3; 1 is ~1% faster at C4 B ≤ 8
 #ifndef L0L2_NMW
 #define L0L2_NMW 14
 #endif

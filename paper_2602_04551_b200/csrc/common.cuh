@@ -128,6 +128,7 @@ struct Ctx {
   int64_t col0 = 0, p_total = 0;
   void* sh_buf = nullptr;
   size_t sh_bytes = 0;
+  Ctx* coop_view = nullptr;   // cooperative ramp-up: this rank's column block as a sharded view (solve.cu)
   void* gemm_ws = nullptr;    // split-K partials of gemm_f64
   size_t gemm_ws_bytes = 0;
 };
@@ -210,7 +211,8 @@ int upper_batch(Ctx* c, int B, const int64_t* supp_off, const int32_t* supp_idx,
 int mp_run(Ctx* c, int max_rounds, cudaStream_t st, std::vector<int32_t>& S_out, std::vector<double>& beta_out,
            double* obj, int* rounds);
 
-void comm_free(Ctx* c);
+void comm_free(Ctx* c);   // also frees the cooperative ramp-up view
+void coop_free(Ctx* c);
 int shard_allreduce(Ctx* c, double* d, int64_t count, cudaStream_t st);   // solve.cu
 int bound_sharded(Ctx* c, int B, const int64_t* fix_off, const int32_t* fix_idx, const uint8_t* fix_val,
                   const double* warm_in, const double* parent_lb, double* lb, double* primal, double* warm_out,

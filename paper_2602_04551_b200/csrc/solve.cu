@@ -99,7 +99,23 @@ int shard_allreduce(Ctx* c, double* d, int64_t count, cudaStream_t st) {
   return L0L2_OK;
 }
 
+// the cooperative ramp-up's column view (coop_view below): only what the view allocated itself (its
+// X, Z, c, L and communicator belong to the full context)
+void coop_free(Ctx* c) {
+  Ctx* v = c->coop_view;
+  if (!v) return;
+  cudaDeviceSynchronize();
+  for (void* q : v->owned) cudaFree(q);
+  for (void* q : v->scr) if (q) cudaFree(q);
+  if (v->sh_buf) cudaFree(v->sh_buf);
+  if (v->gemm_ws) cudaFree(v->gemm_ws);
+  for (auto e : v->ev) if (e) cudaEventDestroy(e);
+  delete v;
+  c->coop_view = nullptr;
+}
+
 void comm_free(Ctx* c) {
+  coop_free(c);
   if (c->nccl && c->nccl_comm) c->nccl->CommDestroy((ncclComm_t)c->nccl_comm);
   c->nccl_comm = nullptr;
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
@@ -230,6 +246,49 @@ std::vector<int64_t> rebalance_plan(const std::vector<int64_t>& counts, int64_t 
 }
 
 namespace {
+
+// ---- cooperative ramp-up: before the frontier is partitioned every rank holds
+// the same tree, so instead of solving the same nodes W times the ranks solve each node once TOGETHER
+// through the column-sharded bound (sharded.cu) on their column block of the full context's Z.
+// Column block r = [cut(r), cut(r+1)): multiples of 8 (a block's padding columns must be zero — only
+// the last block has any, the context's own zero padding).
+int64_t coop_cut(const Ctx* c, int r) {
+  const int64_t p8 = round8(c->p);
+  return std::min<int64_t>(c->p, round8(p8 * r / c->nranks));
+}
+bool coop_possible(const Ctx* c) {
+  for (int r = 0; r < c->nranks; r++)
+    if (coop_cut(c, r + 1) - coop_cut(c, r) < (int64_t)kPt) return false;
+  return true;
+}
+// the rank's block as a column-sharded view: X, Z, c, colsq, L point INTO the full context (no copies);
+// its own ADMM work space; the full context's communicator
+int coop_view(Ctx* c, Ctx** out) {
+  Ctx* v = c->coop_view;
+  if (v && (v->rank != c->rank || v->p_total != c->p)) {
+    coop_free(c);
+    v = nullptr;
+  }
+  if (!v) {
+    v = new Ctx();
+    const int64_t col0 = coop_cut(c, c->rank), col1 = coop_cut(c, c->rank + 1);
+    v->device = c->device; v->sms = c->sms; v->n = c->n; v->p = col1 - col0; v->ld = c->ld;
+    v->lam0 = c->lam0; v->lam2 = c->lam2; v->M = c->M; v->rho = c->rho; v->node_tol = c->node_tol;
+    v->int_tol = c->int_tol; v->check_every = c->check_every; v->max_iters = c->max_iters; v->yy = c->yy;
+    v->X = c->X + col0 * c->ld; v->Z = c->Z + col0 * c->ld; v->y = c->y; v->c = c->c + col0;
+    v->colsq = c->colsq + col0; v->L = c->L; v->Lt = c->Lt;
+    v->sharded = 1; v->col0 = col0; v->p_total = c->p; v->direct = 0;
+    v->nranks = c->nranks; v->rank = c->rank;
+    c->coop_view = v;
+    const int rc = admm_alloc(v);   // the fused step-mode kernel when n fits, else the GEMM loop
+    v->shard_fused = (rc == L0L2_OK && !v->wide) ? 1 : 0;
+    v->err.clear();
+  }
+  // the communicator may have been (re)initialised since: always the full context's
+  v->nccl = c->nccl; v->nccl_comm = c->nccl_comm; v->host_tr = c->host_tr; v->host_tr_set = c->host_tr_set;
+  *out = v;
+  return L0L2_OK;
+}
 
 struct Solver {
   Ctx* c;
@@ -404,7 +463,14 @@ struct Solver {
     // the parents' warm states have been consumed by pack_group
     for (int k = 0; k < B; k++) pool.release(batch[k].slot);
     t_bound += secs(t0);
-    // ---- upper bounds on the rounded supports of the nodes that finished
+    return finish_upper(batch, res, hlb, hpr, hit, hbr, hfl, hlbb);
+  }
+
+  // upper bounds on the rounded supports of the nodes that finished, then the per-node results
+  int finish_upper(std::vector<Node>& batch, std::vector<Res>& res, const std::vector<double>& hlb,
+                   const std::vector<double>& hpr, const std::vector<int32_t>& hit, const std::vector<int32_t>& hbr,
+                   const std::vector<uint8_t>& hfl, const std::vector<double>& hlbb) {
+    const int B = (int)batch.size();
     auto t1 = Clock::now();
     std::vector<int64_t> so(B + 1, 0);
     std::vector<int32_t> sall;
@@ -444,6 +510,162 @@ struct Solver {
     }
     t_upper += secs(t1);
     return L0L2_OK;
+  }
+
+  // Cooperative bound of a batch that every rank holds (ramp-up): rank r runs the node relaxations on its
+  // column block through the column-sharded path (one all-reduce of u = Σ_r Z_r w_r per iteration, the
+  // check totals all-reduced: identical LB / primal / iterations / flags on every rank), the blocks of
+  // the final (β, v) are all-gathered into full warm states, then finalize (branch, integrality,
+  // support) and the upper bounds run on the full context — so every rank derives the same tree.
+  int64_t coop_rounds = 0;
+  int process_coop(std::vector<Node>& batch, std::vector<Res>& res) {
+    const int B = (int)batch.size();
+    res.assign(B, Res{});
+    if (B == 0) return L0L2_OK;
+    auto t0 = Clock::now();
+    coop_rounds++;
+    Ctx* v = nullptr;
+    int rc = coop_view(c, &v);
+    if (rc) return rc;
+    const int64_t p = c->p, pr = v->p, col0 = v->col0;
+    int64_t pmax = 0;
+    for (int r = 0; r < W; r++) pmax = std::max(pmax, coop_cut(c, r + 1) - coop_cut(c, r));
+    std::vector<double> hlb(B), hpr(B);
+    std::vector<int32_t> hit(B), hbr(B);
+    std::vector<uint8_t> hfl(B);
+    std::vector<double> mine((size_t)B * 2 * pmax, 0.0);   // [node][β | v][pmax]: this rank's block
+    for (int pass = 0; pass < 2; pass++) {   // nodes without a parent state (cold), then warm ones
+      std::vector<int> ids;
+      for (int k = 0; k < B; k++) if ((batch[k].slot < 0) == (pass == 0)) ids.push_back(k);
+      if (ids.empty()) continue;
+      const int nb = (int)ids.size();
+      std::vector<int64_t> off(nb + 1, 0);
+      std::vector<int32_t> fidx;
+      std::vector<uint8_t> fval;
+      std::vector<double> plb(nb);
+      for (int i = 0; i < nb; i++) {
+        const Node& u = batch[ids[i]];
+        fidx.insert(fidx.end(), u.fidx.begin(), u.fidx.end());
+        fval.insert(fval.end(), u.fval.begin(), u.fval.end());
+        off[i + 1] = (int64_t)fidx.size();
+        plb[i] = u.lb;
+      }
+      const size_t nw = (size_t)nb * 2 * pr;
+      const size_t bytes = sizeof(int64_t) * (nb + 1) + sizeof(double) * (3 * nb + 2 * nw) + sizeof(int32_t) * nb +
+                           sizeof(int32_t) * std::max<size_t>(1, fidx.size()) + nb + fval.size() + 256;
+      char* blk = (char*)c->scratch_n(2, bytes);
+      if (!blk) return set_err(c, L0L2_ENOMEM, "cooperative bound buffers");
+      int64_t* d_off = (int64_t*)blk;
+      double* d_plb = (double*)(d_off + nb + 1);
+      double* d_lb = d_plb + nb;
+      double* d_pr = d_lb + nb;
+      double* d_win = d_pr + nb;
+      double* d_wout = d_win + nw;
+      int32_t* d_it = (int32_t*)(d_wout + nw);
+      int32_t* d_fi = d_it + nb;
+      uint8_t* d_fl = (uint8_t*)(d_fi + std::max<size_t>(1, fidx.size()));
+      uint8_t* d_fv = d_fl + nb;
+      L0L2_CUDA(c, cudaMemcpyAsync(d_off, off.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, st));
+      L0L2_CUDA(c, cudaMemcpyAsync(d_plb, plb.data(), sizeof(double) * nb, cudaMemcpyHostToDevice, st));
+      if (!fidx.empty()) {
+        L0L2_CUDA(c, cudaMemcpyAsync(d_fi, fidx.data(), sizeof(int32_t) * fidx.size(), cudaMemcpyHostToDevice, st));
+        L0L2_CUDA(c, cudaMemcpyAsync(d_fv, fval.data(), fval.size(), cudaMemcpyHostToDevice, st));
+      }
+      if (pass == 1)   // the parents' (β, v) on this rank's block
+        for (int i = 0; i < nb; i++) {
+          const double* ps = pool.ptr(batch[ids[i]].slot);
+          L0L2_CUDA(c, cudaMemcpyAsync(d_win + (size_t)i * 2 * pr, ps + col0, sizeof(double) * pr,
+                                       cudaMemcpyDeviceToDevice, st));
+          L0L2_CUDA(c, cudaMemcpyAsync(d_win + (size_t)i * 2 * pr + pr, ps + p + col0, sizeof(double) * pr,
+                                       cudaMemcpyDeviceToDevice, st));
+        }
+      rc = bound_sharded(v, nb, d_off, d_fi, d_fv, pass == 1 ? d_win : nullptr, d_plb, d_lb, d_pr, d_wout, d_it,
+                         d_fl, st);
+      if (rc < 0) return set_err(c, rc, "cooperative bound: %s", v->err.c_str());
+      std::vector<double> tlb(nb), tpr(nb), tw(nw);
+      std::vector<int32_t> tit(nb);
+      std::vector<uint8_t> tfl(nb);
+      L0L2_CUDA(c, cudaMemcpyAsync(tlb.data(), d_lb, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
+      L0L2_CUDA(c, cudaMemcpyAsync(tpr.data(), d_pr, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
+      L0L2_CUDA(c, cudaMemcpyAsync(tit.data(), d_it, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+      L0L2_CUDA(c, cudaMemcpyAsync(tfl.data(), d_fl, nb, cudaMemcpyDeviceToHost, st));
+      L0L2_CUDA(c, cudaMemcpyAsync(tw.data(), d_wout, sizeof(double) * nw, cudaMemcpyDeviceToHost, st));
+      L0L2_CUDA(c, cudaStreamSynchronize(st));
+      for (int i = 0; i < nb; i++) {
+        const int k = ids[i];
+        hlb[k] = tlb[i];
+        hpr[k] = tpr[i];
+        hit[k] = tit[i];
+        hfl[k] = tfl[i];
+        std::memcpy(&mine[((size_t)k * 2) * pmax], &tw[(size_t)i * 2 * pr], sizeof(double) * pr);
+        std::memcpy(&mine[((size_t)k * 2 + 1) * pmax], &tw[(size_t)i * 2 * pr + pr], sizeof(double) * pr);
+      }
+    }
+    // every rank's blocks of every node's (β, v)
+    std::vector<double> all((size_t)W * B * 2 * pmax);
+    {
+      auto tc = Clock::now();
+      if ((rc = xg_allgather(mine.data(), all.data(), sizeof(double) * mine.size()))) return rc;
+      t_comm += secs(tc);
+    }
+    // full warm states → fresh pool slots (a full pool: a scratch state, the children start cold)
+    std::vector<int64_t> off(B + 1, 0);
+    std::vector<int32_t> fidx;
+    std::vector<uint8_t> fval;
+    for (int k = 0; k < B; k++) {
+      fidx.insert(fidx.end(), batch[k].fidx.begin(), batch[k].fidx.end());
+      fval.insert(fval.end(), batch[k].fval.begin(), batch[k].fval.end());
+      off[k + 1] = (int64_t)fidx.size();
+    }
+    int32_t* dfi = (int32_t*)c->scratch_n(2, sizeof(int32_t) * std::max<size_t>(1, fidx.size()));
+    uint8_t* dfv = (uint8_t*)c->scratch_n(3, std::max<size_t>(1, fval.size()) + sizeof(double) * 2 * p * kBC + 256);
+    if (!dfi || !dfv) return set_err(c, L0L2_ENOMEM, "cooperative finalize buffers");
+    double* tmp = (double*)(dfv + (std::max<size_t>(1, fval.size()) + 255) / 256 * 256);   // kBC × 2p
+    L0L2_CUDA(c, cudaMemcpyAsync(d.fix_off, off.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
+    if (!fidx.empty()) {
+      L0L2_CUDA(c, cudaMemcpyAsync(dfi, fidx.data(), sizeof(int32_t) * fidx.size(), cudaMemcpyHostToDevice, st));
+      L0L2_CUDA(c, cudaMemcpyAsync(dfv, fval.data(), fval.size(), cudaMemcpyHostToDevice, st));
+    }
+    L0L2_CUDA(c, cudaMemcpyAsync(d.flags, hfl.data(), B, cudaMemcpyHostToDevice, st));
+    std::vector<double> full(2 * p);
+    std::vector<int32_t> scnt(B);
+    for (int g0 = 0; g0 < B; g0 += kBC) {
+      const int nb = std::min(kBC, B - g0);
+      double* hp[2 * kBC] = {};
+      for (int k = 0; k < nb; k++) {
+        for (int r = 0; r < W; r++) {
+          const int64_t a = coop_cut(c, r), b = coop_cut(c, r + 1);
+          const double* src = &all[(((size_t)r * B + g0 + k) * 2) * pmax];
+          std::memcpy(&full[a], src, sizeof(double) * (b - a));
+          std::memcpy(&full[p + a], src + pmax, sizeof(double) * (b - a));
+        }
+        double* t = tmp + (size_t)k * 2 * p;
+        L0L2_CUDA(c, cudaMemcpyAsync(t, full.data(), sizeof(double) * 2 * p, cudaMemcpyHostToDevice, st));
+        L0L2_CUDA(c, cudaStreamSynchronize(st));   // `full` is reused for the next node
+        const int s2 = pool.alloc();
+        res[g0 + k].slot = s2;
+        if (s2 >= 0)
+          L0L2_CUDA(c, cudaMemcpyAsync(pool.ptr(s2), t, sizeof(double) * 2 * p, cudaMemcpyDeviceToDevice, st));
+        hp[k] = t;
+      }
+      L0L2_CUDA(c, cudaMemcpyAsync(d.wptr, hp, sizeof(hp), cudaMemcpyHostToDevice, st));
+      if ((rc = pack_group(c, nb, d.fix_off + g0, dfi, dfv, (const double* const*)d.wptr, st))) return rc;
+      if ((rc = finalize_group(c, nb, nullptr, d.branch + g0, d.flags + g0, d.scnt + g0, d.sidx, p, st))) return rc;
+      L0L2_CUDA(c, cudaMemcpyAsync(scnt.data() + g0, d.scnt + g0, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+      L0L2_CUDA(c, cudaStreamSynchronize(st));
+      for (int k = 0; k < nb; k++) {
+        res[g0 + k].supp.resize(scnt[g0 + k]);
+        if (scnt[g0 + k] > 0)
+          L0L2_CUDA(c, cudaMemcpyAsync(res[g0 + k].supp.data(), d.sidx + (int64_t)k * p, sizeof(int32_t) * scnt[g0 + k],
+                                       cudaMemcpyDeviceToHost, st));
+      }
+    }
+    L0L2_CUDA(c, cudaMemcpyAsync(hbr.data(), d.branch, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaMemcpyAsync(hfl.data(), d.flags, B, cudaMemcpyDeviceToHost, st));
+    L0L2_CUDA(c, cudaStreamSynchronize(st));
+    for (int k = 0; k < B; k++) pool.release(batch[k].slot);   // the parents' states were consumed
+    t_bound += secs(t0);
+    return finish_upper(batch, res, hlb, hpr, hit, hbr, hfl, hlb);
   }
 
   // Algorithm 1 body for one solved batch (id order; UB first, then prune/branch)
@@ -757,6 +979,7 @@ void l0l2_default_solve_opts(l0l2_solve_opts* o) {
   o->init_mp = 0;
   o->early_prune = 0;
   o->continuous = 0;
+  o->coop_rampup = 0;
 }
 
 int l0l2_nccl_unique_id(uint8_t out[128]) {
@@ -964,7 +1187,8 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
     }
     S.rounds++;
     std::vector<Solver::Res> res;
-    if ((rc = S.process(batch, res))) return rc;
+    const bool coop = S.W > 1 && !S.partitioned && o.coop_rampup && coop_possible(c);
+    if ((rc = coop ? S.process_coop(batch, res) : S.process(batch, res))) return rc;
     tt = Clock::now();
     S.update_tree(batch, res);
     S.t_tree += secs(tt);
@@ -1002,6 +1226,7 @@ int l0l2_solve(l0l2_ctx* ctx, const l0l2_solve_opts* opts_in, double* beta, doub
     stats->node_iters_global = S.node_iters;
     stats->nodes_moved = S.moved;
     stats->suspensions = S.suspensions;
+    stats->coop_rounds = S.coop_rounds;
     if (S.W > 1) {
       stats->nodes_moved = 0;
       for (int r = 0; r < S.W; r++) stats->nodes_moved += (int64_t)all[r].pad;

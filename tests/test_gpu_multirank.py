@@ -108,3 +108,23 @@ def test_two_ranks_time_limited_prefix_is_valid():
         assert obj >= ref["obj"] * (1 - 1e-9)
         assert abs(O.ub_objective(P, S, beta[S]) - obj) <= 1e-9 * abs(obj)   # β* attains the reported objective
         assert st["lb"] <= ref["obj"] * (1 + 1e-9)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_cooperative_rampup_certificate_equals_oracle(world):
+    """coop_rampup: until the frontier is partitioned the ranks solve each node
+    together through the column-sharded bound on their column blocks of Z, all-gather the blocks of
+    (β, v) into full warm states and finalize on the full context.  The certificate must still be the
+    oracle's, every rank must return the same β*, and the ramp-up rounds must have run cooperatively."""
+    inst, lam0, lam2, M = _instance()
+    P = O.Problem(inst.X, inst.y, lam0, lam2, M)
+    ref = O.bnb_solve(P, B=8, gap_tol=1e-6, node_tol=1e-8)
+    out = _run(world, dict(gap_tol=1e-6, batch=8, rebalance_every=2, coop_rampup=True))
+    for rank, obj, beta, gap, st, _ in out:
+        assert np.array_equal(np.nonzero(beta)[0], ref["support"]), rank
+        assert abs(obj - ref["obj"]) <= 1e-9 * abs(ref["obj"]), (rank, obj, ref["obj"])
+        assert gap <= 1e-6
+        assert st["lb"] <= ref["obj"] * (1 + 1e-9)
+        assert np.array_equal(beta, out[0][2])
+        assert st["coop_rounds"] >= 1, st
+        assert st["coop_rounds"] == out[0][4]["coop_rounds"]   # the ramp-up is the same on every rank
