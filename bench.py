@@ -682,6 +682,7 @@ def main():
                 "nodes_per_step": nodes_step, "node_iters_per_s": iters_total / (ms / 1e3),
                 "certified_gap": last["gap"], "objective": last["obj"], "support": [int(j) for j in last["support"]],
                 "solve_status": st["status"], "rounds": st["rounds"], "max_open": st["max_open"],
+                "coop_rampup_rounds": st.get("coop_rounds", 0),
                 "phase_s": {"bound": st["t_bound"], "upper": st["t_upper"], "tree": st["t_tree"], "comm": st["t_comm"]},
                 "create_s": t_create, "gpu_launches": int(launches), "device_bytes": int(info["device_bytes"]),
                 "roofline": roof, "upper_bound_kernel": upper, "e2e": e2e, "clocks": clk.summary()}
