@@ -1344,16 +1344,16 @@ __global__ void step_outputs(KP k) {
 // of n×8 Z tiles in shared memory, which caps n at 1056.  Beyond that (the paper's n = 3000 and
 // 11 962 workloads) the SAME iteration runs on the same node state (stt, node_f/node_i,
 // bchk) as a host-stepped sequence:
-//   wide_sweep   S_J = Z_Jᵀu for 64 columns per CTA (DMMA, K = n split over 8 warps, u read from L2,
-//                fixed-order cross-warp tree), then the fused kernel's elementwise epilogue (b, β⁺, v⁺,
-//                w⁺, check terms) — one read of Z;
-//   gemm_f64     u⁺ = Z w⁺ (n × 16, K = p, deterministic split-K) — the second read of Z;
-//   at checks    Xβ⁺ (GEMM) for ‖Xβ‖², then wide_decide: dual, primal, running
-//                max (R7), stop (R8), early prune (R16) — the fused kernel's decision arithmetic.
+//   wide_sweep_p    S_J = Z_Jᵀu for groups of 32 columns (persistent, one CTA per SM; per-warp cp.async
+//                   rings, DMMA, fixed-order cross-warp tree), then the fused kernel's elementwise
+//                   epilogue (b, β⁺, v⁺, w⁺, check terms) — one read of Z;
+//   wide_forward_p  u⁺ = Z w⁺ (n × 16, K = p; row blocks × column chunks, chunk partials summed in
+//                   order by wide_reduce) — the second read of Z;
+//   at checks       Xβ⁺ by the same product on X (‖Xβ‖²), then wide_decide: dual, primal
+//                   (P:320-325), running max (R7), stop (R8), early prune (R16) — the fused
+//                   kernel's decision arithmetic.
 // Z is streamed twice per iteration instead of once; every sum has a fixed order.
-constexpr int WT = 8;                 // 8-column tiles per CTA of wide_sweep
-constexpr int WTH = 256;              // 8 warps
-constexpr int WEL = WT * kPt * kBC;   // (column, node) elements per CTA
+constexpr int WTH = 256;              // 8 warps per CTA
 
 // w = c + ρβ − v of the active nodes (0 for the others), [p8][kBC]; keeps the nodes' starting
 // iteration counts (a resumed node continues its count)
@@ -1371,163 +1371,8 @@ __global__ void __launch_bounds__(WTH) wide_w0(KP k, double* W, int* it0) {
   W[e] = w;
 }
 
-template <bool REFRESH>
-__global__ void __launch_bounds__(WTH) wide_sweep(KP k, int check, double* W, double* Bb, double* wsum) {
-  __shared__ double red[4][WEL];        // cross-warp partials of S (32 KB)
-  __shared__ double csum[WTH / kBC][kBC][4];
-  __shared__ int fl[kBC];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < kBC) fl[tid] = k.nodei[tid * 2];
-  __syncthreads();
-  const int t0 = blockIdx.x * WT;
-  const int nt = min(WT, k.ntiles - t0);
-  const int cA = lane >> 2, kA = lane & 3;
-  // ---- adjoint S_J = Z_Jᵀ u for the CTA's tiles: A = Z_Jᵀ (8 cols × 4 rows), B = u (4 rows × 8 nodes);
-  // warp w takes the k-steps ≡ w (mod 8)
-  double acc[WT][2][2];
-#pragma unroll
-  for (int t = 0; t < WT; t++) acc[t][0][0] = acc[t][0][1] = acc[t][1][0] = acc[t][1][1] = 0.0;
-  {
-    const bool a0 = (fl[cA] & F_ACTIVE) != 0, a1 = (fl[8 + cA] & F_ACTIVE) != 0;
-    const double* U0 = k.U + (int64_t)cA * k.ld + kA;
-    const double* U1 = k.U + (int64_t)(8 + cA) * k.ld + kA;
-    const double* Zb = k.Z + ((int64_t)t0 * kPt + cA) * k.ld + kA;
-    const int kt = (int)((k.n + 3) / 4);   // rows past n: Z and u are zero there (ld ≥ round8(n))
-#pragma unroll 2
-    for (int q = warp; q < kt; q += WTH / 32) {
-      const double u0 = a0 ? __ldcg(U0 + 4 * q) : 0.0;
-      const double u1 = a1 ? __ldcg(U1 + 4 * q) : 0.0;
-      double a[WT];
-#pragma unroll
-      for (int t = 0; t < WT; t++) a[t] = t < nt ? __ldcs(Zb + (int64_t)t * kPt * k.ld + 4 * q) : 0.0;
-#pragma unroll
-      for (int t = 0; t < WT; t++) {
-        dmma(acc[t][0], a[t], u0);
-        dmma(acc[t][1], a[t], u1);
-      }
-    }
-  }
-  // fixed-order tree over the 8 warps: (w, w+4), then (w, w+2), then (w, w+1)
-  auto put = [&](double* dst) {
-#pragma unroll
-    for (int t = 0; t < WT; t++)
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        dst[t * 128 + cA * kBC + 8 * h + 2 * kA] = acc[t][h][0];
-        dst[t * 128 + cA * kBC + 8 * h + 2 * kA + 1] = acc[t][h][1];
-      }
-  };
-  for (int half = 4; half >= 1; half >>= 1) {
-    if (warp >= half && warp < 2 * half) put(red[warp - half]);
-    __syncthreads();
-    if (warp < half) {
-      const double* src = red[warp];
-#pragma unroll
-      for (int t = 0; t < WT; t++)
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          acc[t][h][0] += src[t * 128 + cA * kBC + 8 * h + 2 * kA];
-          acc[t][h][1] += src[t * 128 + cA * kBC + 8 * h + 2 * kA + 1];
-        }
-    }
-    __syncthreads();
-  }
-  if (warp == 0) put(red[0]);
-  __syncthreads();
-  // ---- epilogue (the fused sweep's arithmetic): thread tid owns node tid % 16 of 4 columns
-  const int node = tid & (kBC - 1);
-  const bool active = (fl[node] & F_ACTIVE) != 0, cold = (fl[node] & F_COLD) != 0;
-  double sT1 = 0.0, sT2 = 0.0, sT3 = 0.0, sT4 = 0.0;
-#pragma unroll
-  for (int i = 0; i < WEL / WTH; i++) {
-    const int e = tid + WTH * i, t = e >> 7, el = e & 127, jj = el >> 4;
-    if (t >= nt) continue;
-    const int64_t tile = t0 + t, col = tile * kPt + jj;
-    double* q = k.stt + tile * STQ;
-    const double q_beta = q[el], q_v = q[STB + el], q_c = q[2 * STB + jj];
-    const uint8_t q_code = reinterpret_cast<const uint8_t*>(q + 2 * STB + 8)[el];
-    const double sv = red[0][e];
-    const double w = q_c + k.rho * q_beta - q_v;
-    double wn = 0.0, bo = 0.0;
-    if (active) {
-      const double b = (w - sv) * k.inv_rho;                          // b = D w, D = (I − ZᵀZ)/ρ (R1)
-      const double bn = REFRESH ? q_beta : prox(k, b + q_v * k.inv_rho, q_code);
-      const double vn = (REFRESH && cold) ? q_v : q_v + k.rho * (b - bn);   // cold: (0, 0), no refresh (R6)
-      if (check) {
-        sT1 = fma(b, sv, sT1);                                        // bᵀ(XᵀX b)
-        sT2 += nu_f(k, fabs(q_c - sv), q_code);                      // Σ ν(|Xᵀr̂|)
-        sT3 = fma(q_c, bn, sT3);                                      // cᵀβ
-        sT4 += psi_f(k, bn, q_code);                                  // Σ ψ(β)
-        k.bchk[col * kBC + node] = b;
-      }
-      q[el] = bn;
-      q[STB + el] = vn;
-      wn = q_c + k.rho * bn - vn;
-      bo = bn;
-    }
-    W[col * kBC + node] = wn;
-    if (check) Bb[col * kBC + node] = bo;
-  }
-  if (!check) return;
-  csum[tid >> 4][node][0] = sT1;
-  csum[tid >> 4][node][1] = sT2;
-  csum[tid >> 4][node][2] = sT3;
-  csum[tid >> 4][node][3] = sT4;
-  __syncthreads();
-  if (tid < kBC * 4) {
-    const int nd = tid >> 2, term = tid & 3;
-    double a = 0.0;
-    for (int g = 0; g < WTH / kBC; g++) a += csum[g][nd][term];
-    wsum[((int64_t)blockIdx.x * kBC + nd) * 4 + term] = a;
-  }
-}
-
-// Forward product for the wide-n path: dst = A W (n × 16, K = p) for A = Z (u⁺ = Z w⁺) or X (Xβ⁺ at
-// checks).  CTA (x, y) owns rows [512x, 512x + 512) and the column chunk y; each warp 64 rows (8 DMMA
-// row tiles × 2 node halves in registers), k-steps of 4 columns streamed from HBM once; the chunk
-// partials are summed in chunk order by wide_reduce (deterministic).
-constexpr int WFR = 512;
-__global__ void __launch_bounds__(WTH) wide_forward(const double* __restrict__ A, int64_t ld, int64_t n, int64_t p8,
-                                                    const double* __restrict__ W, int64_t cpc, double* part) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, cA = lane >> 2, kA = lane & 3;
-  const int64_t r0 = (int64_t)blockIdx.x * WFR + warp * 64;
-  const int64_t c0 = (int64_t)blockIdx.y * cpc, c1 = min(p8, c0 + cpc);
-  double acc[8][2][2];
-  bool rv[8];
-#pragma unroll
-  for (int i = 0; i < 8; i++) {
-    acc[i][0][0] = acc[i][0][1] = acc[i][1][0] = acc[i][1][1] = 0.0;
-    rv[i] = r0 + 8 * i + cA < n;
-  }
-  const double* Ab = A + (c0 + kA) * ld + r0 + cA;
-  const double* Wb = W + (c0 + kA) * kBC + cA;
-#pragma unroll 2
-  for (int64_t c = c0; c < c1; c += 4) {
-    const int64_t o = (c - c0);
-    const double b0 = __ldg(Wb + o * kBC), b1 = __ldg(Wb + o * kBC + 8);
-    double a[8];
-#pragma unroll
-    for (int i = 0; i < 8; i++) a[i] = rv[i] ? __ldcs(Ab + o * ld + 8 * i) : 0.0;
-#pragma unroll
-    for (int i = 0; i < 8; i++) {
-      dmma(acc[i][0], a[i], b0);
-      dmma(acc[i][1], a[i], b1);
-    }
-  }
-  double* pb = part + (int64_t)blockIdx.y * kBC * ld;
-#pragma unroll
-  for (int i = 0; i < 8; i++) {
-    if (!rv[i]) continue;
-    const int64_t row = r0 + 8 * i + cA;
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      pb[(int64_t)(8 * h + 2 * kA) * ld + row] = acc[i][h][0];
-      pb[(int64_t)(8 * h + 2 * kA + 1) * ld + row] = acc[i][h][1];
-    }
-  }
-}
-// ---- pipelined variants (default): each warp streams its share of Z through its own cp.async ring in
-// shared memory (no registers held by loads in flight, no CTA barrier inside the K loop), one CTA per SM.
+// Each warp streams its share of Z through its own cp.async ring in shared memory (no registers held
+// by loads in flight, no CTA barrier inside the K loop), one CTA per SM.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr(dst)), "l"(src), "r"(src_bytes) : "memory");
 }
@@ -1938,22 +1783,13 @@ int admm_alloc_wide(Ctx* c) {
   c->wXB = (double*)dalloc(c, sizeof(double) * kBC * ld);
   c->wsum = (double*)dalloc(c, sizeof(double) * nblk * kBC * 4);
   c->wit0 = (int*)dalloc(c, sizeof(int) * kBC);
-  c->wide_v1 = 0;
-  if (const char* e = getenv("L0L2_WIDE_V1")) c->wide_v1 = atoi(e) != 0;   // tuning hook: register-prefetch kernels
-  if (c->wide_v1) {
-    // forward grid: row blocks × column chunks (≥ 64 columns each, a multiple of 4), ≈ 2 CTAs per SM
-    c->wrb = (int)((c->n + WFR - 1) / WFR);
-    c->wcc = (int)std::max<int64_t>(1, std::min<int64_t>(p8 / 64, (2 * c->sms + c->wrb - 1) / c->wrb));
-    c->wcpc = ((p8 + c->wcc - 1) / c->wcc + 3) / 4 * 4;
-  } else {
-    // one CTA per SM: row blocks × column chunks ≤ #SMs (chunks ≥ 64 columns, a multiple of a stage)
-    c->wrb = (int)((round8(c->n) + WFPR - 1) / WFPR);
-    c->wcc = (int)std::max<int64_t>(1, std::min<int64_t>(p8 / 64, c->sms / c->wrb));
-    c->wcpc = ((p8 + c->wcc - 1) / c->wcc + WFPC - 1) / WFPC * WFPC;
-    L0L2_CUDA(c, cudaFuncSetAttribute(wide_sweep_p<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSWEEP_SMEM));
-    L0L2_CUDA(c, cudaFuncSetAttribute(wide_sweep_p<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSWEEP_SMEM));
-    L0L2_CUDA(c, cudaFuncSetAttribute(wide_forward_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WFWD_SMEM));
-  }
+  // forward grid, one CTA per SM: row blocks × column chunks ≤ #SMs (chunks ≥ 64 columns, whole stages)
+  c->wrb = (int)((round8(c->n) + WFPR - 1) / WFPR);
+  c->wcc = (int)std::max<int64_t>(1, std::min<int64_t>(p8 / 64, c->sms / c->wrb));
+  c->wcpc = ((p8 + c->wcc - 1) / c->wcc + WFPC - 1) / WFPC * WFPC;
+  L0L2_CUDA(c, cudaFuncSetAttribute(wide_sweep_p<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSWEEP_SMEM));
+  L0L2_CUDA(c, cudaFuncSetAttribute(wide_sweep_p<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSWEEP_SMEM));
+  L0L2_CUDA(c, cudaFuncSetAttribute(wide_forward_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WFWD_SMEM));
   c->wcc = (int)((p8 + c->wcpc - 1) / c->wcpc);
   c->wpart = (double*)dalloc(c, sizeof(double) * c->wcc * kBC * ld);
   c->node_f = (double*)dalloc(c, sizeof(double) * kBC * 4);
@@ -2153,25 +1989,17 @@ int run_admm_wide(Ctx* c, const BoundArgs& a, cudaStream_t st) {
                                c->node_i);
   L0L2_LAUNCHED(c);
   const KP k = make_kp(c, a, mask);
-  const int nblk = c->wide_v1 ? (k.ntiles + WT - 1) / WT : (k.ntiles + WGT - 1) / WGT;   // check-sum blocks
-  const unsigned sgrid = c->wide_v1 ? (unsigned)nblk : (unsigned)std::min(nblk, c->sms);
+  const int nblk = (k.ntiles + WGT - 1) / WGT;   // check-sum blocks = column groups of the sweep
+  const unsigned sgrid = (unsigned)std::min(nblk, c->sms);
   auto sweep = [&](bool refresh, int chk) {
-    if (c->wide_v1) {
-      if (refresh) wide_sweep<true><<<sgrid, WTH, 0, st>>>(k, chk, c->wW, c->wB, c->wsum);
-      else wide_sweep<false><<<sgrid, WTH, 0, st>>>(k, chk, c->wW, c->wB, c->wsum);
-    } else {
-      if (refresh) wide_sweep_p<true><<<sgrid, WTH, WSWEEP_SMEM, st>>>(k, chk, c->wW, c->wB, c->wsum);
-      else wide_sweep_p<false><<<sgrid, WTH, WSWEEP_SMEM, st>>>(k, chk, c->wW, c->wB, c->wsum);
-    }
+    if (refresh) wide_sweep_p<true><<<sgrid, WTH, WSWEEP_SMEM, st>>>(k, chk, c->wW, c->wB, c->wsum);
+    else wide_sweep_p<false><<<sgrid, WTH, WSWEEP_SMEM, st>>>(k, chk, c->wW, c->wB, c->wsum);
     L0L2_LAUNCHED(c);
     return L0L2_OK;
   };
   auto forward_of = [&](const double* A, const double* W, double* dst) {   // dst = A W (n × 16, K = p)
-    if (c->wide_v1)
-      wide_forward<<<dim3((unsigned)c->wrb, (unsigned)c->wcc), WTH, 0, st>>>(A, c->ld, c->n, k.p8, W, c->wcpc, c->wpart);
-    else
-      wide_forward_p<<<dim3((unsigned)c->wrb, (unsigned)c->wcc), WTH, WFWD_SMEM, st>>>(A, c->ld, k.n8, k.p8, W, c->wcpc,
-                                                                                        c->wpart);
+    wide_forward_p<<<dim3((unsigned)c->wrb, (unsigned)c->wcc), WTH, WFWD_SMEM, st>>>(A, c->ld, k.n8, k.p8, W, c->wcpc,
+                                                                                      c->wpart);
     L0L2_LAUNCHED(c);
     wide_reduce<<<(unsigned)((c->n * kBC + 255) / 256), 256, 0, st>>>(c->n, c->ld, c->wcc, c->wpart, dst);
     L0L2_LAUNCHED(c);

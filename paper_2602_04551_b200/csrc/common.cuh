@@ -78,7 +78,6 @@ struct Ctx {
   int *wit0 = nullptr;                                      // iterations of the nodes before the launch
   double *wpart = nullptr;                                  // forward partials per column chunk [wcc][kBC][ld]
   int wrb = 0, wcc = 0;                                     // forward grid: row blocks × column chunks
-  int wide_v1 = 0;                                          // register-prefetch kernels instead of cp.async rings
   int64_t wcpc = 0;                                         // columns per chunk
   // scratch for batch I/O in solve (device)
   std::vector<void*> owned;
