@@ -1380,7 +1380,7 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-constexpr int WPS = 4;                       // ring stages per warp
+constexpr int WPS = 4;                       // ring stages per warp (5 measured slower at B = 16: 0.50 vs 0.41 ms)
 constexpr int WGT = 4;                       // tiles per group of the pipelined sweep (32 columns)
 constexpr int WGC = WGT * kPt;               // 32 columns
 constexpr int WGE = WGC * kBC;               // (column, node) elements per group
