@@ -92,7 +92,7 @@ def ncu_traffic():
     try:
         # the ratio measured on a tree-step launch of this very step (tools/ncu_tree_step.py +
         # tools/ncu_summary.py), else the round-1 fixed-iteration capture
-        for name in ("ncu_admm_tree_launch_r02.json", "ncu_admm_traffic.json"):
+        for name in ("ncu_admm_tree_launch_r02b.json", "ncu_admm_tree_launch_r02.json", "ncu_admm_traffic.json"):
             pth = os.path.join(ROOT, "profiles", name)
             if os.path.exists(pth):
                 with open(pth) as f:
