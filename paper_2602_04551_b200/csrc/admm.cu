@@ -1442,8 +1442,10 @@ __global__ void __launch_bounds__(WTH, 1) wide_sweep_p(KP k, int check, double* 
     const int64_t row0 = (int64_t)(warp + NWP * sI) * WSR;
 #pragma unroll
     for (int ks = 0; ks < 4; ks++) {
-      xa[ks] = (a0 && nsw > 0) ? __ldcg(Ur0 + row0 + 4 * ks) : 0.0;
-      xb[ks] = (a1 && nsw > 0) ? __ldcg(Ur1 + row0 + 4 * ks) : 0.0;
+      // the last stage may run past n8 (and past ld): those rows of Z are zero-filled, u is not read
+      const bool rv = nsw > 0 && row0 + 4 * ks + kA < k.n8;
+      xa[ks] = (a0 && rv) ? __ldcg(Ur0 + row0 + 4 * ks) : 0.0;
+      xb[ks] = (a1 && rv) ? __ldcg(Ur1 + row0 + 4 * ks) : 0.0;
     }
   };
   // u rows two stages ahead, rotating three register sets (L2 latency under full HBM load exceeds one
