@@ -63,8 +63,6 @@ struct KP {
   // order, then a dense per-node list in CTA order
   int32_t* seg_idx; double* seg_val; int* seg_cnt;   // [grid][kBC][seg_cap], [grid][kBC]
   int32_t* nz_idx; double* nz_val;                     // [kBC][nz_cap]
-  uint8_t* nzmap;                                      // [2][p8]: column has a β⁺ nonzero in node half h
-                                                       // (written by the epilogue at check sweeps)
   const double* __restrict__ X;                        // column-major, ld
   int seg_cap, nz_cap;
   double* nodef;                   // [kBC][4]: lb_best, primal, parent_lb, last dual
@@ -91,7 +89,6 @@ struct KP {
   int step_mode, step_phase, step_chk;
   double* tot_out;                 // [kBC][4] this rank's Σ of the check terms (phase 2, check)
   int compact;                     // node-slot compaction allowed (tuning / test hook)
-  int gather_mode;                 // primal check: 0 = union gather (fallback per-node), 1 = per-node gather
   int pfs;                         // tiles L2-prefetched by prefill (during the grid reduction)
   int tsplit;                      // bulk copies per Z tile (divides kPt)
   double rho, inv_rho, lam0, lam2, M, yy, node_tol;
@@ -647,8 +644,6 @@ __device__ void sweep(const KP& k, Smem& s, bool refresh, bool check, unsigned& 
           // append this tile's nonzeros of β⁺ to the (sub-range, epilogue warp, node) segment, in
           // column order: ballot + popcount, no barrier (every lane of a node keeps the same count)
           const unsigned bal = __ballot_sync(0xffffffffu, bnz != 0.0);
-          // union of the half's nonzero columns (gather_union): lane nd = 0 of each column
-          if (nd == 0) k.nzmap[(int64_t)h * k.p8 + col0 + j] = ((bal >> (8 * ((tid & 31) >> 3))) & 0xFFu) ? 1 : 0;
           const unsigned mnode = bal & (0x01010101u << nd);
           if (bnz != 0.0) {
             const int r = seg_n + __popc(mnode & ((1u << (tid & 31)) - 1u));
@@ -831,125 +826,6 @@ __device__ void gather_partial(const KP& k, Smem& s, const int* tot) {
 
 // ‖L (Zβ)‖² partials: rows of L split over CTAs; per node one partial per CTA (nodes whose β⁺
 // has more than nz_cap nonzeros; the others use gather_partial).
-// ‖Xβ⁺‖² of every active node over this CTA's rows, reading each column of X that is nonzero in ANY
-// active node once (the per-node gather above reads a column once per node holding it: 16× the bytes
-// when the nodes of a group share their supports, as siblings do).  The union of the nonzero columns
-// (the epilogue's per-half maps) becomes a sorted list in the idle tile ring (every CTA builds the same
-// list); warp w sums, for 4 nodes × 8 rows, the column quarter w/4 of the list SEQUENTIALLY in column
-// order, and the 4 quarter sums are added in quarter order: a node's sum runs over its own nonzeros
-// in a fixed order plus exact zeros (fma(x, 0, a) = a), so it does not depend on the other nodes.
-// Returns false (nothing written, ring untouched) when the union does not fit the ring.
-__device__ bool gather_union(const KP& k, Smem& s) {
-  const int g = blockIdx.x, G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int a0 = 0, a1 = 0;
-  for (int nd = 0; nd < 8; nd++) { a0 |= s.flags[nd] & F_ACTIVE; a1 |= s.flags[8 + nd] & F_ACTIVE; }
-  const int nwd = (int)((k.p8 + 31) / 32);
-  const int64_t ring_words = (int64_t)NST * kPt * k.ld * 2;
-  const int64_t cap = ring_words - nwd - 64;
-  uint32_t* bm = reinterpret_cast<uint32_t*>(s.tiles);
-  int* lst = reinterpret_cast<int*>(bm + nwd);
-  __shared__ int wsum[kAdmmThreads / 32], qb[5], tot_u;
-  // bitmap of the union (one word = 32 columns per thread pass)
-  int cnt = 0;
-  for (int w = tid; w < nwd; w += blockDim.x) {
-    uint32_t word = 0;
-    for (int b = 0; b < 32; b++) {
-      const int64_t j = (int64_t)w * 32 + b;
-      if (j < k.p8) {
-        const uint8_t m = (a0 ? __ldcg(k.nzmap + j) : 0) | (a1 ? __ldcg(k.nzmap + k.p8 + j) : 0);
-        word |= (m ? 1u : 0u) << b;
-      }
-    }
-    bm[w] = word;
-    cnt += __popc(word);
-  }
-  // block-wide total (and per-thread exclusive offsets for the list below)
-  int incl = cnt;
-  for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= o) incl += v; }
-  if (lane == 31) wsum[warp] = incl;
-  __syncthreads();
-  if (tid == 0) {
-    int a = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) { const int v = wsum[w]; wsum[w] = a; a += v; }
-    tot_u = a;
-  }
-  __syncthreads();
-  if (tot_u > cap) {   // (the same decision in every CTA: the maps are the same)
-    for (int w = tid; w < nwd; w += blockDim.x) bm[w] = 0u;
-    if (tid < NST) s.zres[tid] = -1;
-    __syncthreads();
-    return false;
-  }
-  // sorted list: thread tid owns words tid, tid + blockDim, ... — write its entries at its offset,
-  // in word order; the offset of a thread's k-th word needs the counts of all earlier words, so the
-  // list is written in rounds of blockDim words
-  {
-    int base = 0;
-    for (int w0 = 0; w0 < nwd; w0 += blockDim.x) {
-      const int w = w0 + tid;
-      const uint32_t word = w < nwd ? bm[w] : 0u;
-      const int c = __popc(word);
-      int inc = c;
-      for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += v; }
-      __syncthreads();
-      if (lane == 31) wsum[warp] = inc;
-      __syncthreads();
-      int pre = 0, all = 0;
-      for (int ww = 0; ww < (int)(blockDim.x >> 5); ww++) { if (ww < warp) pre += wsum[ww]; all += wsum[ww]; }
-      int pos = base + pre + inc - c;
-      uint32_t x = word;
-      while (x) {
-        const int b = __ffs(x) - 1;
-        lst[pos++] = w * 32 + b;
-        x &= x - 1;
-      }
-      base += all;
-    }
-  }
-  __syncthreads();
-  // quarter boundaries of the list: columns [q·p8/4, (q+1)·p8/4)
-  if (tid < 5) {
-    const int64_t lim = k.p8 * tid / 4;
-    int lo = 0, hi = tot_u;
-    while (lo < hi) { const int mid = (lo + hi) >> 1; if (lst[mid] < lim) lo = mid + 1; else hi = mid; }
-    qb[tid] = lo;
-  }
-  __syncthreads();
-  const int64_t i0 = k.xn * g / G, i1 = k.xn * (g + 1) / G;
-  const int q = warp >> 2, node = 4 * (warp & 3) + (lane >> 3), r = lane & 7;
-  const bool act = (s.flags[node] & F_ACTIVE) != 0;
-  double* red = s.spart;   // [4 quarters][8 rows][16 nodes]
-  double part = 0.0;       // thread tid < kBC: node tid
-  for (int64_t r0 = i0; r0 < i1; r0 += 8) {
-    const int64_t row = r0 + r;
-    double acc = 0.0;
-    if (act && row < i1) {
-      const double* xr = k.X + row;
-#pragma unroll 4
-      for (int e = qb[q]; e < qb[q + 1]; e++) {
-        const int64_t j = lst[e];
-        acc = fma(__ldg(xr + j * k.xld), __ldcg(k.stt + st_beta(j, node)), acc);
-      }
-    }
-    red[(q * 8 + r) * kBC + node] = acc;
-    __syncthreads();
-    if (tid < kBC && (s.flags[tid] & F_ACTIVE))
-      for (int rr = 0; rr < 8 && r0 + rr < i1; rr++) {
-        const double xb = ((red[(0 * 8 + rr) * kBC + tid] + red[(1 * 8 + rr) * kBC + tid]) +
-                           red[(2 * 8 + rr) * kBC + tid]) + red[(3 * 8 + rr) * kBC + tid];
-        part = fma(xb, xb, part);
-      }
-    __syncthreads();
-  }
-  if (tid < kBC && (s.flags[tid] & F_ACTIVE)) k.sums2[(int64_t)g * kBC + tid] = part;
-  // give the ring back: zeros (the MMA warps' fragment loads past n8 must read finite data) and no
-  // resident tile (the next sweep re-stages its tiles)
-  for (int64_t w = tid; w < nwd + tot_u; w += blockDim.x) bm[w] = 0u;
-  if (tid < NST) s.zres[tid] = -1;
-  __syncthreads();
-  return true;
-}
-
 __device__ void lmatvec_partial(const KP& k, Smem& s) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = blockIdx.x, G = gridDim.x;
@@ -1146,7 +1022,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k_in) {
     PROF_RESET();
     // primal ‖Xβ‖²: a gather over β⁺'s nonzeros (sparse at the paper's workloads); a node with
     // more than nz_cap nonzeros falls back to one forward-only sweep Zβ and ‖L(Zβ)‖²
-    if (!(k.gather_mode == 0 && gather_union(k, s))) {
+    {
       gather_partial(k, s, tot_s);
       bool dense = false;
       if (tid < kBC) s.ncnt[tid] = tot_s[tid];
@@ -1973,8 +1849,6 @@ int admm_alloc(Ctx* c) {
   c->seg_cnt = (int*)dalloc(c, sizeof(int) * c->grid * NEW * kBC);
   c->nz_idx = (int32_t*)dalloc(c, sizeof(int32_t) * kBC * c->nz_cap);
   c->nz_val = (double*)dalloc(c, sizeof(double) * kBC * c->nz_cap);
-  c->nzmap = (uint8_t*)dalloc(c, 2 * (size_t)p8);
-  if (c->nzmap) L0L2_CUDA(c, cudaMemset(c->nzmap, 0, 2 * (size_t)p8));
   if (!c->seg_idx || !c->seg_val || !c->seg_cnt || !c->nz_idx || !c->nz_val)
     return set_err(c, L0L2_ENOMEM, "sparse check work space");
   c->node_f = (double*)dalloc(c, sizeof(double) * kBC * 4);
@@ -2183,9 +2057,7 @@ KP make_kp(Ctx* c, const BoundArgs& a, unsigned mask) {
   k.U = c->U; k.Ub = c->Ub; k.Upart = c->Upart; k.sums = c->sums; k.sums2 = c->sums2;
   k.nodef = c->node_f; k.nodei = c->node_i; k.bar = c->bar;
   k.seg_idx = c->seg_idx; k.seg_val = c->seg_val; k.seg_cnt = c->seg_cnt; k.nz_idx = c->nz_idx; k.nz_val = c->nz_val;
-  k.X = c->X; k.seg_cap = c->seg_cap; k.nz_cap = c->nz_cap; k.nzmap = c->nzmap;
-  k.gather_mode = 0;
-  if (const char* e = getenv("L0L2_GATHER")) k.gather_mode = atoi(e) != 0;   // test hook: 1 = per-node gather
+  k.X = c->X; k.seg_cap = c->seg_cap; k.nz_cap = c->nz_cap;
   // testing hook (0 = always the dense sweep); the direct regime has no dense fallback (it needs Z)
   if (const char* e = getenv("L0L2_NZCAP"))
     if (!c->direct) k.nz_cap = std::min(k.nz_cap, atoi(e));

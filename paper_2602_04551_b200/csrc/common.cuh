@@ -54,7 +54,6 @@ struct Ctx {
   double *seg_val = nullptr, *nz_val = nullptr;
   int *seg_cnt = nullptr;
   int seg_cap = 0, nz_cap = 0;
-  uint8_t* nzmap = nullptr;                                 // [2][p8] union of β⁺ nonzero columns (admm.cu)
 
   // matching-pursuit root heuristic work space (mp.cu, allocated on first use)
   double *mp_r = nullptr, *mp_beta = nullptr, *mp_log = nullptr;

@@ -1,5 +1,5 @@
 """Per-warp phase breakdown of admm_persistent from a -DL0L2_PROF build (developer tool):
-    L0L2_LIB=libl0l2_prof.so python tools/prof_phases.py C4 200 16"""
+    L0L2_LIB=libl0l2_prof.so python tools/prof_phases.py C4 200 16 [check_every]"""
 import ctypes as C
 import sys
 
@@ -13,9 +13,11 @@ from paper_2602_04551_b200 import Problem, binding  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 nb = int(sys.argv[3]) if len(sys.argv) > 3 else 16
+ce = int(sys.argv[4]) if len(sys.argv) > 4 else 10
 inst = synth.config_instance(cfg, seed=0)
 rho = 3.0 * float(np.mean(np.einsum("ij,ij->j", inst.X, inst.X)))
-pr = Problem(inst.X, inst.y, inst.lambda0, inst.lambda2, inst.M, rho=rho, node_tol=-1.0, max_iters=iters)
+pr = Problem(inst.X, inst.y, inst.lambda0, inst.lambda2, inst.M, rho=rho, node_tol=-1.0, max_iters=iters,
+             check_every=ce)
 fx = [((), ())] + synth.random_fixings(inst.p, nb - 1, seed=5, depth_lo=1, depth_hi=6, prefer=inst.support_true)
 lib = binding.load_library()
 buf = (C.c_ulonglong * (160 * 16 * 8))()
