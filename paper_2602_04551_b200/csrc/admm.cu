@@ -89,6 +89,7 @@ struct KP {
   int step_mode, step_phase, step_chk;
   double* tot_out;                 // [kBC][4] this rank's Σ of the check terms (phase 2, check)
   int compact;                     // node-slot compaction allowed (tuning / test hook)
+  int gather_mode;                 // primal check gather: 0 = whole columns (Z-form), 1 = row slices
   int pfs;                         // tiles L2-prefetched by prefill (during the grid reduction)
   int tsplit;                      // bulk copies per Z tile (divides kPt)
   double rho, inv_rho, lam0, lam2, M, yy, node_tol;
@@ -826,6 +827,46 @@ __device__ void gather_partial(const KP& k, Smem& s, const int* tot) {
 
 // ‖L (Zβ)‖² partials: rows of L split over CTAs; per node one partial per CTA (nodes whose β⁺
 // has more than nz_cap nonzeros; the others use gather_partial).
+// Column-partitioned primal gather (Z-form): CTA g takes the g-th of G equal chunks of every active,
+// non-dense node's nonzero list and accumulates X_j β_j over WHOLE columns (8n-byte coalesced reads)
+// into its forward-partial slot Upart[g][node][·]; reduce_u then sums the slots in CTA order (fixed
+// order; a node's chunks depend on its own nonzero count only) and xnorm_partial takes ‖Xβ‖² over the
+// CTA's rows.  Compared with gather_partial (each CTA gathers its ~n/G rows of every nonzero column:
+// 64-byte pieces) this reads X in full columns at the price of two grid barriers.
+__device__ void gather_cols(const KP& k, Smem& s, const int* tot) {
+  const int g = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
+  for (int nd = 0; nd < kBC; nd++) {
+    if (!(s.flags[nd] & F_ACTIVE) || tot[nd] > k.nz_cap) continue;   // (the same in every thread)
+    const int cnt = tot[nd];
+    const int e0 = (int)((int64_t)cnt * g / G), e1 = (int)((int64_t)cnt * (g + 1) / G);
+    const int32_t* ix = k.nz_idx + (int64_t)nd * k.nz_cap;
+    const double* vx = k.nz_val + (int64_t)nd * k.nz_cap;
+    double* up = k.Upart + ((int64_t)g * kBC + nd) * k.ld;
+    for (int64_t i = tid; i < k.n8; i += blockDim.x) {   // rows n..n8 of X are zero padding
+      double a = 0.0;
+#pragma unroll 4
+      for (int e = e0; e < e1; e++) a = fma(__ldcg(vx + e), __ldg(k.X + (int64_t)__ldcg(ix + e) * k.xld + i), a);
+      up[i] = a;
+    }
+  }
+}
+__device__ void xnorm_partial(const KP& k, Smem& s, const int* tot) {
+  const int g = blockIdx.x, G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = k.xn * g / G, i1 = k.xn * (g + 1) / G;
+  // warp w: node w (16 warps = 16 nodes), rows of the slice strided by lane, then a fixed butterfly
+  const int nd = warp;
+  double part = 0.0;
+  if (nd < kBC && (s.flags[nd] & F_ACTIVE) && tot[nd] <= k.nz_cap) {
+    for (int64_t i = i0 + lane; i < i1; i += 32) {
+      const double x = __ldcg(k.Ub + (int64_t)nd * k.ld + i);
+      part = fma(x, x, part);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) k.sums2[(int64_t)g * kBC + nd] = part;
+  }
+}
+
 __device__ void lmatvec_partial(const KP& k, Smem& s) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = blockIdx.x, G = gridDim.x;
@@ -1023,7 +1064,15 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k_in) {
     // primal ‖Xβ‖²: a gather over β⁺'s nonzeros (sparse at the paper's workloads); a node with
     // more than nz_cap nonzeros falls back to one forward-only sweep Zβ and ‖L(Zβ)‖²
     {
-      gather_partial(k, s, tot_s);
+      if (!DIR && k.gather_mode == 0) {   // whole-column gather (Z-form: Upart holds ≥ n rows)
+        gather_cols(k, s, tot_s);
+        grid_sync(k.bar);
+        reduce_u(k, s, k.Ub);
+        grid_sync(k.bar);
+        xnorm_partial(k, s, tot_s);
+      } else {
+        gather_partial(k, s, tot_s);
+      }
       bool dense = false;
       if (tid < kBC) s.ncnt[tid] = tot_s[tid];
       __syncthreads();
@@ -2058,6 +2107,10 @@ KP make_kp(Ctx* c, const BoundArgs& a, unsigned mask) {
   k.nodef = c->node_f; k.nodei = c->node_i; k.bar = c->bar;
   k.seg_idx = c->seg_idx; k.seg_val = c->seg_val; k.seg_cnt = c->seg_cnt; k.nz_idx = c->nz_idx; k.nz_val = c->nz_val;
   k.X = c->X; k.seg_cap = c->seg_cap; k.nz_cap = c->nz_cap;
+  // whole-column gather where it measured faster: C4 (p = 1e5) 130 vs 173 µs per check at B = 16, the
+  // step +1.1%; at C3 (p = 1e4) its two extra grid barriers cost more than it saves (107 vs 91 µs)
+  k.gather_mode = (c->p >= 32768) ? 0 : 1;
+  if (const char* e = getenv("L0L2_GATHER")) k.gather_mode = atoi(e) != 0;   // test / tuning hook
   // testing hook (0 = always the dense sweep); the direct regime has no dense fallback (it needs Z)
   if (const char* e = getenv("L0L2_NZCAP"))
     if (!c->direct) k.nz_cap = std::min(k.nz_cap, atoi(e));

@@ -152,6 +152,28 @@ def test_compaction_is_bitwise_invisible(case, monkeypatch):
     prob.close()
 
 
+def test_column_gather_equals_row_gather(case, monkeypatch):
+    """The primal check's ‖Xβ⁺‖²: the whole-column gather (default in the Z-form) and the row-slice
+    gather (L0L2_GATHER=1) agree to rounding with the same iteration counts and decisions, and the
+    default keeps a node's result independent of the other nodes (one node alone = the same node in
+    a 16-node batch, bitwise)."""
+    name, inst, lam0, lam2, M, P = case
+    prob = Problem(inst.X, inst.y, lam0, lam2, M, rho=P.rho, node_tol=1e-7, max_iters=800)
+    fx = _fixings(inst, 16, seed=9)
+    monkeypatch.setenv("L0L2_GATHER", "0")
+    a = prob.l0l2_bound_batch(fx)
+    single = prob.l0l2_bound_batch(fx[5:6])
+    monkeypatch.setenv("L0L2_GATHER", "1")
+    b = prob.l0l2_bound_batch(fx)
+    assert torch.equal(a["iters"], b["iters"]) and torch.equal(a["branch_j"], b["branch_j"])
+    for key in ("lb", "primal"):
+        x, y = a[key].cpu().numpy(), b[key].cpu().numpy()
+        assert np.all(np.abs(x - y) <= 1e-12 * np.maximum(1.0, np.abs(y))), key
+    for key in ("warm_out", "lb", "primal", "iters", "flags"):
+        assert torch.equal(a[key][5:6], single[key]), key
+    prob.close()
+
+
 def test_converged_bounds_and_decisions(case):
     """T3: converged LB / primal within 1e-6; LB ≤ independent relaxation optimum; iteration
     counts, branch index and support equal where the decisions are separated."""
