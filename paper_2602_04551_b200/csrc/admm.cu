@@ -827,36 +827,40 @@ __device__ void gather_partial(const KP& k, Smem& s, const int* tot) {
 
 // ‖L (Zβ)‖² partials: rows of L split over CTAs; per node one partial per CTA (nodes whose β⁺
 // has more than nz_cap nonzeros; the others use gather_partial).
-// Column-partitioned primal gather (Z-form): CTA g takes the g-th of G equal chunks of every active,
-// non-dense node's nonzero list and accumulates X_j β_j over WHOLE columns (8n-byte coalesced reads)
-// into its forward-partial slot Upart[g][node][·]; reduce_u then sums the slots in CTA order (fixed
-// order; a node's chunks depend on its own nonzero count only) and xnorm_partial takes ‖Xβ‖² over the
-// CTA's rows.  Compared with gather_partial (each CTA gathers its ~n/G rows of every nonzero column:
-// 64-byte pieces) this reads X in full columns at the price of two grid barriers.
-__device__ void gather_cols(const KP& k, Smem& s, const int* tot) {
-  const int g = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
+// Column-partitioned primal gather (Z-form): CTA g accumulates X_j β_j over WHOLE columns (8n-byte
+// coalesced reads) for the β⁺ nonzeros of sub-range g — the epilogue's own segments (sub-range g,
+// epilogue warp 0 then 1, column order within each), no compaction into per-node lists — of every
+// active node into the forward-partial slot Upart[g][node][·]; reduce_u then sums the slots in
+// sub-range order (the forward partials' fixed order, so a node's sum depends on its own nonzeros only)
+// and xnorm_partial takes ‖Xβ‖² over the CTA's rows.  No per-node cap: no dense Zβ fallback.
+__device__ void gather_segs(const KP& k, Smem& s) {
+  const int g = blockIdx.x, tid = threadIdx.x;
   for (int nd = 0; nd < kBC; nd++) {
-    if (!(s.flags[nd] & F_ACTIVE) || tot[nd] > k.nz_cap) continue;   // (the same in every thread)
-    const int cnt = tot[nd];
-    const int e0 = (int)((int64_t)cnt * g / G), e1 = (int)((int64_t)cnt * (g + 1) / G);
-    const int32_t* ix = k.nz_idx + (int64_t)nd * k.nz_cap;
-    const double* vx = k.nz_val + (int64_t)nd * k.nz_cap;
+    if (!(s.flags[nd] & F_ACTIVE)) continue;   // (the same in every thread)
+    const int64_t q0 = ((int64_t)g * NEW + 0) * kBC + nd, q1 = ((int64_t)g * NEW + 1) * kBC + nd;
+    const int c0 = __ldcg(k.seg_cnt + q0), c1 = __ldcg(k.seg_cnt + q1);
+    const int32_t* i0p = k.seg_idx + q0 * k.seg_cap;
+    const int32_t* i1p = k.seg_idx + q1 * k.seg_cap;
+    const double* v0p = k.seg_val + q0 * k.seg_cap;
+    const double* v1p = k.seg_val + q1 * k.seg_cap;
     double* up = k.Upart + ((int64_t)g * kBC + nd) * k.ld;
     for (int64_t i = tid; i < k.n8; i += blockDim.x) {   // rows n..n8 of X are zero padding
       double a = 0.0;
 #pragma unroll 4
-      for (int e = e0; e < e1; e++) a = fma(__ldcg(vx + e), __ldg(k.X + (int64_t)__ldcg(ix + e) * k.xld + i), a);
+      for (int e = 0; e < c0; e++) a = fma(__ldcg(v0p + e), __ldg(k.X + (int64_t)__ldcg(i0p + e) * k.xld + i), a);
+#pragma unroll 4
+      for (int e = 0; e < c1; e++) a = fma(__ldcg(v1p + e), __ldg(k.X + (int64_t)__ldcg(i1p + e) * k.xld + i), a);
       up[i] = a;
     }
   }
 }
-__device__ void xnorm_partial(const KP& k, Smem& s, const int* tot) {
+__device__ void xnorm_partial(const KP& k, Smem& s) {
   const int g = blockIdx.x, G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t i0 = k.xn * g / G, i1 = k.xn * (g + 1) / G;
   // warp w: node w (16 warps = 16 nodes), rows of the slice strided by lane, then a fixed butterfly
   const int nd = warp;
   double part = 0.0;
-  if (nd < kBC && (s.flags[nd] & F_ACTIVE) && tot[nd] <= k.nz_cap) {
+  if (nd < kBC && (s.flags[nd] & F_ACTIVE)) {
     for (int64_t i = i0 + lane; i < i1; i += 32) {
       const double x = __ldcg(k.Ub + (int64_t)nd * k.ld + i);
       part = fma(x, x, part);
@@ -1054,7 +1058,8 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k_in) {
     grid_sync(k.bar);
     if (!DIR) reduce_u(k, s, k.U);
     __shared__ int tot_s[kBC];
-    if (chk) compact_nonzeros(k, s, tot_s);   // β⁺'s nonzeros → dense per-node lists
+    const bool segs = !DIR && k.gather_mode == 0;   // primal from the segments (gather_segs)
+    if (chk && !segs) compact_nonzeros(k, s, tot_s);   // β⁺'s nonzeros → dense per-node lists
     // (direct regime, no check: w⁺ is complete after the first barrier and the next sweep writes the
     // other buffer, so one barrier per iteration suffices)
     if (!DIR || chk) grid_sync(k.bar);
@@ -1063,16 +1068,14 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k_in) {
     PROF_RESET();
     // primal ‖Xβ‖²: a gather over β⁺'s nonzeros (sparse at the paper's workloads); a node with
     // more than nz_cap nonzeros falls back to one forward-only sweep Zβ and ‖L(Zβ)‖²
-    {
-      if (!DIR && k.gather_mode == 0) {   // whole-column gather (Z-form: Upart holds ≥ n rows)
-        gather_cols(k, s, tot_s);
-        grid_sync(k.bar);
-        reduce_u(k, s, k.Ub);
-        grid_sync(k.bar);
-        xnorm_partial(k, s, tot_s);
-      } else {
-        gather_partial(k, s, tot_s);
-      }
+    if (segs) {   // whole-column gather from the segments (Z-form: Upart holds ≥ n rows)
+      gather_segs(k, s);
+      grid_sync(k.bar);
+      reduce_u(k, s, k.Ub);
+      grid_sync(k.bar);
+      xnorm_partial(k, s);
+    } else {
+      gather_partial(k, s, tot_s);
       bool dense = false;
       if (tid < kBC) s.ncnt[tid] = tot_s[tid];
       __syncthreads();
@@ -2107,8 +2110,9 @@ KP make_kp(Ctx* c, const BoundArgs& a, unsigned mask) {
   k.nodef = c->node_f; k.nodei = c->node_i; k.bar = c->bar;
   k.seg_idx = c->seg_idx; k.seg_val = c->seg_val; k.seg_cnt = c->seg_cnt; k.nz_idx = c->nz_idx; k.nz_val = c->nz_val;
   k.X = c->X; k.seg_cap = c->seg_cap; k.nz_cap = c->nz_cap;
-  // whole-column gather where it measured faster: C4 (p = 1e5) 130 vs 173 µs per check at B = 16, the
-  // step +1.1%; at C3 (p = 1e4) its two extra grid barriers cost more than it saves (107 vs 91 µs)
+  // whole-column gather from the segments where it measured faster: C4 (p = 1e5) 133 vs 173 µs per
+  // check at B = 16, the step +1.1%; at C3 (p = 1e4) its two extra grid barriers cost more than it
+  // saves (108 vs 91 µs)
   k.gather_mode = (c->p >= 32768) ? 0 : 1;
   if (const char* e = getenv("L0L2_GATHER")) k.gather_mode = atoi(e) != 0;   // test / tuning hook
   // testing hook (0 = always the dense sweep); the direct regime has no dense fallback (it needs Z)

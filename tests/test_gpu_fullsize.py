@@ -109,6 +109,7 @@ def test_dense_primal_fallback(monkeypatch):
     """L0L2_NZCAP = 0 forces the dense-β⁺ primal check (forward-only sweep Zβ, reduction,
     ‖L(Zβ)‖²) for every node at every check: same fixed-iteration bounds as the oracle."""
     monkeypatch.setenv("L0L2_NZCAP", "0")
+    monkeypatch.setenv("L0L2_GATHER", "1")   # the row-slice gather path (whose dense fallback this is)
     inst = synth.make_instance(200, 2000, 5, 0.1, 3.0, 3)   # p > 2n: Z-form
     lam2 = max(synth.tune_lambda2(inst), 0.5)
     inst.lambda2 = lam2

@@ -153,10 +153,11 @@ def test_compaction_is_bitwise_invisible(case, monkeypatch):
 
 
 def test_column_gather_equals_row_gather(case, monkeypatch):
-    """The primal check's ‖Xβ⁺‖²: the whole-column gather (default in the Z-form) and the row-slice
-    gather (L0L2_GATHER=1) agree to rounding with the same iteration counts and decisions, and the
-    default keeps a node's result independent of the other nodes (one node alone = the same node in
-    a 16-node batch, bitwise)."""
+    """The primal check's ‖Xβ⁺‖²: the whole-column gather from the epilogue's segments (default in the
+    Z-form, no compaction, no dense fallback) and the row-slice gather over compacted per-node lists
+    (L0L2_GATHER=1) agree to rounding with the same iteration counts and decisions, and the default
+    keeps a node's result independent of the other nodes (one node alone = the same node in a
+    16-node batch, bitwise)."""
     name, inst, lam0, lam2, M, P = case
     prob = Problem(inst.X, inst.y, lam0, lam2, M, rho=P.rho, node_tol=1e-7, max_iters=800)
     fx = _fixings(inst, 16, seed=9)
