@@ -217,6 +217,11 @@ int64_t l0l2_solve_trace(const l0l2_ctx* ctx, double* rec, int64_t max_nodes);
 /* Multi-GPU, one process per GPU (torch.distributed provides the process group and
  * broadcasts the id bytes).  NCCL is loaded at run time (libnccl.so.2).             */
 int l0l2_nccl_unique_id(uint8_t out[128]);
+/* Self-test of the NCCL carrier on one rank (device ordinal `device`): loads libnccl.so.2, builds a
+ * 1-rank communicator and runs the collectives the multi-GPU exchange uses — in-place all-reduce of
+ * doubles, all-gather, broadcast, a grouped send/recv to itself — checking the bytes.  L0L2_OK, or
+ * L0L2_ENCCL / L0L2_ECUDA. */
+int l0l2_nccl_selftest(int32_t device);
 int l0l2_comm_init(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id[128]);
 
 /* Alternative to NCCL: a caller-provided HOST transport (e.g. a gloo / MPI process group, or

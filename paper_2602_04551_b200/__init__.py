@@ -8,7 +8,7 @@ inspected), but creating a problem without a CUDA device raises L0L2Error.
 from .binding import (  # noqa: F401
     L0L2Error, Problem, lib_path, load_library, exported_symbols, rebalance_plan,
     FLAG_CONVERGED, FLAG_INTEGRAL, FLAG_MAXITER, FLAG_PRUNED, OK, EINVAL, ENOMEM, ECUDA, ENCCL, WNOTCONV, WLIMIT,
-    nccl_unique_id, HostTransport, ShardedProblem,
+    nccl_unique_id, nccl_selftest, HostTransport, ShardedProblem,
 )
 
 __all__ = ["Problem", "ShardedProblem", "L0L2Error", "load_library", "rebalance_plan"]

@@ -109,6 +109,8 @@ def load_library():
     lib.l0l2_bound_sharded.restype = C.c_int
     lib.l0l2_info.argtypes = [P] + [P] * 5
     lib.l0l2_info.restype = C.c_int
+    lib.l0l2_nccl_selftest.argtypes = [C.c_int32]
+    lib.l0l2_nccl_selftest.restype = C.c_int
     lib.l0l2_admm_path.argtypes = [P]
     lib.l0l2_admm_path.restype = C.c_int
     lib.l0l2_last_error.argtypes = [P]
@@ -143,6 +145,11 @@ def rebalance_plan(counts, batch, max_moves=64):
     if m < 0:
         raise L0L2Error(m, "bad arguments")
     return [tuple(int(x) for x in plan[3 * i:3 * i + 3]) for i in range(min(m, max_moves))]
+
+
+def nccl_selftest(device=0) -> int:
+    """l0l2_nccl_selftest: the NCCL calls of the multi-GPU exchange on a 1-rank communicator."""
+    return load_library().l0l2_nccl_selftest(int(device))
 
 
 def nccl_unique_id() -> bytes:

@@ -993,6 +993,46 @@ int l0l2_nccl_unique_id(uint8_t out[128]) {
   return L0L2_OK;
 }
 
+int l0l2_nccl_selftest(int32_t device) {
+  std::string err;
+  NcclApi* api = load_nccl(err);
+  if (!api) return L0L2_ENCCL;
+  if (cudaSetDevice(device) != cudaSuccess) return L0L2_ECUDA;
+  ncclUniqueId id;
+  if (api->GetUniqueId(&id) != ncclSuccess) return L0L2_ENCCL;
+  ncclComm_t comm = nullptr;
+  if (api->CommInitRank(&comm, 1, id, 0) != ncclSuccess) return L0L2_ENCCL;
+  cudaStream_t st = nullptr;
+  double* d = nullptr;
+  int rc = L0L2_OK;
+  const double h0[8] = {1, 2, 3, 4, 5, 6, 7, 8};
+  double h[32] = {};
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess || cudaMalloc(&d, sizeof(double) * 32) != cudaSuccess)
+    rc = L0L2_ECUDA;
+  // the calls the solver's exchange uses (solve.cu xg_*, shard_allreduce), on one rank: all-reduce in
+  // place, all-gather, broadcast, and a grouped send/recv to itself
+  if (!rc && cudaMemcpyAsync(d, h0, sizeof(h0), cudaMemcpyHostToDevice, st) != cudaSuccess) rc = L0L2_ECUDA;
+  if (!rc && api->AllReduce(d, d, 8, ncclDouble, ncclSum, comm, st) != ncclSuccess) rc = L0L2_ENCCL;
+  if (!rc && api->AllGather(d, d + 8, 8 * sizeof(double), ncclChar, comm, st) != ncclSuccess) rc = L0L2_ENCCL;
+  if (!rc && api->Broadcast(d + 8, d + 16, 8 * sizeof(double), ncclChar, 0, comm, st) != ncclSuccess) rc = L0L2_ENCCL;
+  if (!rc) {
+    if (api->GroupStart() != ncclSuccess) rc = L0L2_ENCCL;
+    if (!rc && api->Send(d + 16, 8 * sizeof(double), ncclChar, 0, comm, st) != ncclSuccess) rc = L0L2_ENCCL;
+    if (!rc && api->Recv(d + 24, 8 * sizeof(double), ncclChar, 0, comm, st) != ncclSuccess) rc = L0L2_ENCCL;
+    if (api->GroupEnd() != ncclSuccess) rc = L0L2_ENCCL;
+  }
+  if (!rc && (cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+              cudaStreamSynchronize(st) != cudaSuccess))
+    rc = L0L2_ECUDA;
+  if (!rc)
+    for (int i = 0; i < 32; i++)
+      if (h[i] != h0[i % 8]) rc = L0L2_ENCCL;
+  if (d) cudaFree(d);
+  if (st) cudaStreamDestroy(st);
+  api->CommDestroy(comm);
+  return rc;
+}
+
 int l0l2_comm_init(l0l2_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id[128]) {
   if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) return L0L2_EINVAL;
   Ctx* c = &ctx->impl;

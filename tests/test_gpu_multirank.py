@@ -128,3 +128,13 @@ def test_cooperative_rampup_certificate_equals_oracle(world):
         assert np.array_equal(beta, out[0][2])
         assert st["coop_rounds"] >= 1, st
         assert st["coop_rounds"] == out[0][4]["coop_rounds"]   # the ramp-up is the same on every rank
+
+
+def test_nccl_carrier_single_rank_selftest():
+    """The NCCL carrier itself (one GPU per rank in production; NCCL refuses two ranks on one device,
+    so the multi-rank tests above use the host transport): libnccl.so.2 loads, a 1-rank communicator
+    forms, and the exchange's collectives (in-place all-reduce, all-gather, broadcast, grouped
+    send/recv) move the right bytes."""
+    from paper_2602_04551_b200 import OK, nccl_selftest
+    torch.cuda.init()
+    assert nccl_selftest(0) == OK
