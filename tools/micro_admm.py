@@ -16,8 +16,10 @@ HBM = 6540.8
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
 Bs = [int(b) for b in (sys.argv[2] if len(sys.argv) > 2 else "1,8,16").split(",")]
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 100
-if cfg == "P3000":   # the paper's n = 3000, p = 30000 workload, wide-n ADMM path
-    inst = synth.make_instance(3000, 30000, 10, 0.1, 10.0 / 3.0, 0)
+if cfg in ("P3000", "P11962"):   # the paper's n = 3000, p = 30000 workload / its real data set's
+    # shape n = 11 962, p = 23 250 (synthetic data of that shape), wide-n ADMM path
+    n_, p_ = (3000, 30000) if cfg == "P3000" else (11962, 23250)
+    inst = synth.make_instance(n_, p_, 10, 0.1, 10.0 / 3.0, 0)
     lam2 = synth.tune_lambda2(inst)
     inst.lambda2, inst.lambda0, inst.M = lam2, synth.lambda0_rule(inst, lam2), synth.bigM_rule(inst, lam2)
 else:
