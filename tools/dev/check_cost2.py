@@ -1,6 +1,7 @@
 """Developer probe: where the convergence check's cost goes at C4 B = 16 (fixed 100 iterations):
 nonzeros of β⁺ per node and their union, and the launch time with check_every 10 / 100 under the
-primal-gather variants (union gather, per-node gather, forced dense Zβ sweep)."""
+primal-gather variants (L0L2_GATHER=0 whole columns from the segments, =1 row slices, and the row
+slices with the dense Zβ sweep forced by L0L2_NZCAP=0)."""
 import json
 import os
 import sys
