@@ -834,43 +834,81 @@ __device__ void gather_partial(const KP& k, Smem& s, const int* tot) {
 // sub-range order (the forward partials' fixed order, so a node's sum depends on its own nonzeros only)
 // and xnorm_partial takes ‖Xβ‖² over the CTA's rows.  No per-node cap: no dense Zβ fallback.
 __device__ void gather_segs(const KP& k, Smem& s) {
-  const int g = blockIdx.x, tid = threadIdx.x;
-  for (int nd = 0; nd < kBC; nd++) {
-    if (!(s.flags[nd] & F_ACTIVE)) continue;   // (the same in every thread)
+  // work items (node, 256-row chunk) dealt to the 16 warps in turn (at B = 1 one node's chunks still
+  // spread over several warps); a lane holds 8 rows 32 apart, so each segment entry issues 8 coalesced
+  // loads per lane; per row the entries are summed in segment order (epilogue warp 0's columns, then
+  // warp 1's), as a sequential walk would
+  const int g = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nchunk = (int)((k.n8 + 255) / 256);
+  for (int it = warp; it < kBC * nchunk; it += kAdmmThreads / 32) {
+    const int nd = it / nchunk;
+    const int64_t r0 = (int64_t)(it % nchunk) * 256;
+    if (!(s.flags[nd] & F_ACTIVE)) continue;
     const int64_t q0 = ((int64_t)g * NEW + 0) * kBC + nd, q1 = ((int64_t)g * NEW + 1) * kBC + nd;
-    const int c0 = __ldcg(k.seg_cnt + q0), c1 = __ldcg(k.seg_cnt + q1);
-    const int32_t* i0p = k.seg_idx + q0 * k.seg_cap;
-    const int32_t* i1p = k.seg_idx + q1 * k.seg_cap;
-    const double* v0p = k.seg_val + q0 * k.seg_cap;
-    const double* v1p = k.seg_val + q1 * k.seg_cap;
+    const int32_t* ixp[2] = {k.seg_idx + q0 * k.seg_cap, k.seg_idx + q1 * k.seg_cap};
+    const double* vxp[2] = {k.seg_val + q0 * k.seg_cap, k.seg_val + q1 * k.seg_cap};
+    const int cn[2] = {__ldcg(k.seg_cnt + q0), __ldcg(k.seg_cnt + q1)};
     double* up = k.Upart + ((int64_t)g * kBC + nd) * k.ld;
-    for (int64_t i = tid; i < k.n8; i += blockDim.x) {   // rows n..n8 of X are zero padding
-      double a = 0.0;
-#pragma unroll 4
-      for (int e = 0; e < c0; e++) a = fma(__ldcg(v0p + e), __ldg(k.X + (int64_t)__ldcg(i0p + e) * k.xld + i), a);
-#pragma unroll 4
-      for (int e = 0; e < c1; e++) a = fma(__ldcg(v1p + e), __ldg(k.X + (int64_t)__ldcg(i1p + e) * k.xld + i), a);
-      up[i] = a;
-    }
+    double a[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) a[r] = 0.0;
+    for (int sgm = 0; sgm < 2; sgm++)
+      for (int e = 0; e < cn[sgm]; e++) {
+        const double v = __ldcg(vxp[sgm] + e);
+        const double* col = k.X + (int64_t)__ldcg(ixp[sgm] + e) * k.xld + r0 + lane;
+#pragma unroll
+        for (int r = 0; r < 8; r++)   // rows n..n8 of X are zero padding
+          if (r0 + lane + 32 * r < k.n8) a[r] = fma(v, __ldg(col + 32 * r), a[r]);
+      }
+#pragma unroll
+    for (int r = 0; r < 8; r++)
+      if (r0 + lane + 32 * r < k.n8) up[r0 + lane + 32 * r] = a[r];
   }
 }
-__device__ void xnorm_partial(const KP& k, Smem& s) {
-  const int g = blockIdx.x, G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t i0 = k.xn * g / G, i1 = k.xn * (g + 1) / G;
-  // warp w: node w (16 warps = 16 nodes), rows of the slice strided by lane, then a fixed butterfly
-  const int nd = warp;
-  double part = 0.0;
-  if (nd < kBC && (s.flags[nd] & F_ACTIVE)) {
-    for (int64_t i = i0 + lane; i < i1; i += 32) {
-      const double x = __ldcg(k.Ub + (int64_t)nd * k.ld + i);
-      part = fma(x, x, part);
+// The gather's partials → Ub for THIS CTA's rows [n8·g/G, n8·(g+1)/G) of every active node (the same
+// per-element order as reduce_u: fixed chunks of the Q partials), then ‖Xβ‖² over those rows per node
+// in row order.  Row ranges, unlike reduce_u's node-major element ranges, do not depend on a node's
+// slot, so a node's result is the same alone or in a batch; no grid barrier between the two steps.
+__device__ void reduce_rows_norm(const KP& k, Smem& s) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = blockIdx.x, G = gridDim.x, Q = k.nsr;
+  const int64_t r0 = k.n8 * g / G, r1 = k.n8 * (g + 1) / G, nr = r1 - r0;
+  const int64_t E = (int64_t)kBC * nr;
+  const int el = tid % RED_E, c = tid / RED_E;
+  const int q0 = Q * c / RED_C, q1 = Q * (c + 1) / RED_C;
+  for (int64_t eb = 0; eb < E; eb += RED_E) {
+    const int64_t e = eb + el;
+    const int64_t nd = nr > 0 ? e / nr : 0, row = r0 + (nr > 0 ? e % nr : 0);
+    double a = 0.0;
+    const bool live = e < E && (s.flags[nd] & F_ACTIVE);
+    if (live) {
+      const double* src = k.Upart + nd * k.ld + row;
+      const int64_t qs = (int64_t)kBC * k.ld;
+      for (int q = q0; q < q1; q++) a += __ldcg(src + q * qs);
     }
+    s.spart[c * RED_E + el] = a;
+    __syncthreads();
+    if (c == 0 && live) {
+      double r = s.spart[el];
+#pragma unroll
+      for (int cc = 1; cc < RED_C; cc++) r += s.spart[cc * RED_E + el];
+      k.Ub[nd * k.ld + row] = r;
+    }
+    __syncthreads();
+  }
+  // warp w ↔ node w: squares over this CTA's rows in row order (lane stride, fixed butterfly)
+  if (warp < kBC && (s.flags[warp] & F_ACTIVE)) {
+    double part = 0.0;
+    for (int64_t i = r0 + lane; i < r1; i += 32)
+      if (i < k.xn) {
+        const double x = __ldcg(k.Ub + (int64_t)warp * k.ld + i);
+        part = fma(x, x, part);
+      }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if (lane == 0) k.sums2[(int64_t)g * kBC + nd] = part;
+    if (lane == 0) k.sums2[(int64_t)g * kBC + warp] = part;
   }
 }
-
 __device__ void lmatvec_partial(const KP& k, Smem& s) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = blockIdx.x, G = gridDim.x;
@@ -1071,9 +1109,7 @@ __global__ void __launch_bounds__(kAdmmThreads, 1) admm_persistent(KP k_in) {
     if (segs) {   // whole-column gather from the segments (Z-form: Upart holds ≥ n rows)
       gather_segs(k, s);
       grid_sync(k.bar);
-      reduce_u(k, s, k.Ub);
-      grid_sync(k.bar);
-      xnorm_partial(k, s);
+      reduce_rows_norm(k, s);   // (the final grid barrier below orders sums2 for the decision)
     } else {
       gather_partial(k, s, tot_s);
       bool dense = false;
