@@ -2146,10 +2146,9 @@ KP make_kp(Ctx* c, const BoundArgs& a, unsigned mask) {
   k.nodef = c->node_f; k.nodei = c->node_i; k.bar = c->bar;
   k.seg_idx = c->seg_idx; k.seg_val = c->seg_val; k.seg_cnt = c->seg_cnt; k.nz_idx = c->nz_idx; k.nz_val = c->nz_val;
   k.X = c->X; k.seg_cap = c->seg_cap; k.nz_cap = c->nz_cap;
-  // whole-column gather from the segments where it measured faster: C4 (p = 1e5) 133 vs 173 µs per
-  // check at B = 16, the step +1.1%; at C3 (p = 1e4) its two extra grid barriers cost more than it
-  // saves (108 vs 91 µs)
-  k.gather_mode = (c->p >= 32768) ? 0 : 1;
+  // whole-column gather from the segments (measured faster at C4, C3 and C5: per 100 iterations at
+  // B = 16, 29.5 vs 30.4 ms, 5.01 vs 5.38 ms, 5.38 vs 5.66 ms); the row-slice gather stays as the hook
+  k.gather_mode = 0;
   if (const char* e = getenv("L0L2_GATHER")) k.gather_mode = atoi(e) != 0;   // test / tuning hook
   // testing hook (0 = always the dense sweep); the direct regime has no dense fallback (it needs Z)
   if (const char* e = getenv("L0L2_NZCAP"))
